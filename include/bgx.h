@@ -1,0 +1,162 @@
+/*
+ * bgx.h — C ABI of libbgx.so, the B200 (sm_100a) execution backend for the
+ * einsum / linalg.generic hot path of arXiv 2503.04771 (reference package
+ * `bridgegen`, pure Python).
+ *
+ * The reference has no native boundary: its only compute engine is
+ * `interp._Machine._generic` (/root/reference/pkg/src/bridgegen/interp.py:372-424),
+ * dispatched from `_Machine.execute` (interp.py:351-352).  Every entry point
+ * below replaces one piece of that loop nest; the Python mirror of the
+ * reference API (paper_2503_04771_b200/interp.py, .../compat.py) classifies a
+ * generic op and calls exactly one of them.  INTEGRATION.md shows the ctypes
+ * binding a bridgegen maintainer would add at interp.py:351.
+ *
+ * Conventions
+ *   - Plain C types only; no torch/CUDA types in signatures.  `stream` is a
+ *     cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - All pointers are DEVICE pointers on the current CUDA device, except the
+ *     descriptor structs themselves (host memory, read during the call only).
+ *   - Strides are in ELEMENTS, may be any non-negative value (views allowed).
+ *   - Return 0 (BGX_OK) or a negative bgx_status; bgx_last_error() returns a
+ *     thread-local message for the last failure on the calling thread.
+ *   - The library never allocates user-visible memory and never frees caller
+ *     memory.  Calls are stream-ordered and asynchronous; thread-safe across
+ *     threads/devices/streams.
+ *   - There is no CPU fallback: an unsupported case returns
+ *     BGX_ERR_UNSUPPORTED and the caller must pick another entry point.
+ */
+#ifndef BGX_H_
+#define BGX_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BGX_API __attribute__((visibility("default")))
+#else
+#define BGX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BGX_VERSION 1
+#define BGX_MAX_RANK 8        /* permute operand rank */
+#define BGX_MAX_AXES 12       /* generic iteration axes */
+#define BGX_MAX_OPERANDS 6    /* generic inputs */
+
+typedef enum {
+  BGX_OK = 0,
+  BGX_ERR_INVALID = -1,      /* bad arguments (shapes, strides, dtypes)       */
+  BGX_ERR_UNSUPPORTED = -2,  /* valid but not handled by this entry point     */
+  BGX_ERR_CUDA = -3,         /* CUDA runtime / driver failure                 */
+  BGX_ERR_NO_DEVICE = -4     /* no sm_100 device visible                      */
+} bgx_status;
+
+/* Element types.  The reference knows only f32/f64 (bridgegen ir.py:71-78);
+ * bf16/f16 are the tensor-core input types of the B200 path. */
+typedef enum { BGX_F32 = 0, BGX_F64 = 1, BGX_BF16 = 2, BGX_F16 = 3 } bgx_dtype;
+
+typedef struct {
+  void *data;                    /* device pointer                              */
+  int32_t dtype;                 /* bgx_dtype                                   */
+  int32_t rank;                  /* 0..BGX_MAX_RANK                             */
+  int64_t shape[BGX_MAX_RANK];
+  int64_t stride[BGX_MAX_RANK];  /* elements                                    */
+} bgx_tensor;
+
+/* ---- library ------------------------------------------------------------ */
+BGX_API int bgx_version(void);
+BGX_API const char *bgx_last_error(void);
+/* Number of SMs of the current device (148 on B200), or a negative status. */
+BGX_API int bgx_sm_count(void);
+
+/* ---- permutation ---------------------------------------------------------
+ * Replaces _generic for a passthrough body (einsum.py:105-108 `return x1`):
+ *   out[i_0..i_{r-1}] = in[j] with j[perm[d]] = i_d, i.e. output dim d reads
+ *   input dim perm[d].  Bit-exact (bytes are moved, never converted).
+ * in/out: same dtype, same rank r, out->shape[d] == in->shape[perm[d]].     */
+BGX_API int bgx_permute(const bgx_tensor *in, const bgx_tensor *out,
+                const int32_t *perm, void *stream);
+
+/* ---- generic loop nest ---------------------------------------------------
+ * Replaces _generic for ANY einsum body (interp.py:372-424 + einsum.py:100-118)
+ * with the reference's exact rounding: one device thread per output element
+ * walks that element's reduction sub-space in the reference's lexicographic
+ * order, p = x1; p = p*xk (k = 2..n); acc = p + acc, each op separately
+ * rounded (no FMA).  Bit-identical to the reference for f32 and f64.
+ * Axes: [0, n_par) are the output (parallel) axes in output order, then the
+ * reduction axes (einsum.py:81).  c0 and out are dense row-major over the
+ * parallel axes; c0 may equal out.  passthrough = (n_in == 1 && no reduction). */
+typedef struct {
+  int32_t n_in;
+  int32_t n_axes;
+  int32_t n_par;
+  int32_t dtype;                                   /* BGX_F32 or BGX_F64  */
+  int64_t extents[BGX_MAX_AXES];
+  const void *ins[BGX_MAX_OPERANDS];
+  int64_t strides[BGX_MAX_OPERANDS][BGX_MAX_AXES]; /* 0 = axis not indexed */
+  const void *c0;
+  void *out;
+} bgx_generic_desc;
+BGX_API int bgx_generic(const bgx_generic_desc *d, void *stream);
+
+/* ---- batched strided contraction (GEMM) ----------------------------------
+ * Replaces _generic for a two-input multiply-accumulate body whose axes
+ * group into batch / M / N / K (each group flattened to one extent by the
+ * caller):
+ *   out[b,m,n] = (c0 ? c0[b,m,n] : 0) + sum_k a[b,m,k] * b[b,k,n]
+ * Kernel selection (bgx_contract_desc.mode):
+ *   BGX_MODE_AUTO    bf16/f16 -> tensor cores (tcgen05) when TMA-legal, else
+ *                    SIMT; f32/f64 -> BGX_MODE_EXACT.
+ *   BGX_MODE_EXACT   f32/f64 CUDA-core tiles, products and sums separately
+ *                    rounded in increasing k: bit-identical to the reference.
+ *   BGX_MODE_FFMA    f32 CUDA-core tiles with fused multiply-add (rel. err
+ *                    <= 1e-5 vs the reference, faster).
+ *   BGX_MODE_TC      tcgen05/TMEM/TMA tensor-core path (bf16/f16 inputs, f32
+ *                    accumulate); BGX_ERR_UNSUPPORTED if not TMA-legal.
+ *   BGX_MODE_SIMT    CUDA-core path for any dtype (f32 accumulate for 16-bit).
+ * Output dtype may be the input dtype or f32 (out_dtype).  The TC path needs
+ * one unit stride in each of a (k or m) and b (k or n), 16-byte aligned base
+ * pointers and 16-byte multiple non-unit strides, and out/c0 n-stride 1.    */
+typedef enum {
+  BGX_MODE_AUTO = 0, BGX_MODE_EXACT = 1, BGX_MODE_FFMA = 2, BGX_MODE_TC = 3,
+  BGX_MODE_SIMT = 4
+} bgx_mode;
+
+typedef struct {
+  int32_t tile_n;     /* 0 = auto; TC: 64/128/256                           */
+  int32_t stages;     /* 0 = auto; TC smem pipeline depth                   */
+  int32_t cta_group;  /* 0 = auto; TC: 1 or 2 (CTA pair, M = 256)           */
+  int32_t max_ctas;   /* 0 = auto (persistent: one CTA per SM)              */
+  int32_t raster;     /* 0 = auto; L2 tile-group width along M              */
+  int32_t reserved[3];
+} bgx_schedule;
+
+typedef struct {
+  int64_t batch, M, N, K;
+  const void *a; int64_t a_stride[3];   /* (batch, m, k) */
+  const void *b; int64_t b_stride[3];   /* (batch, k, n) */
+  const void *c0; int64_t c_stride[3];  /* (batch, m, n); NULL => zero init */
+  void *out; int64_t o_stride[3];       /* (batch, m, n) */
+  int32_t in_dtype;                     /* bgx_dtype of a and b             */
+  int32_t out_dtype;                    /* bgx_dtype of out and c0          */
+  int32_t mode;                         /* bgx_mode                         */
+  int32_t flags;                        /* reserved, 0                      */
+  bgx_schedule sched;
+} bgx_contract_desc;
+BGX_API int bgx_contract(const bgx_contract_desc *d, void *stream);
+/* Which kernel bgx_contract would launch: 1 = tcgen05, 2 = SIMT exact,
+ * 3 = SIMT ffma, 4 = SIMT 16-bit, negative = error. */
+BGX_API int bgx_contract_kernel(const bgx_contract_desc *d);
+
+/* ---- elementwise helpers for multi-GPU K-split -------------------------
+ * out[i] = (dtype_out) src[i] for n elements, src f32 (the reduced partials),
+ * out f32/bf16/f16; with c0 != NULL adds c0[i] first (in f32).           */
+BGX_API int bgx_cast_f32(const float *src, const void *c0, void *out, int32_t out_dtype,
+                 int64_t n, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGX_H_ */

@@ -1,0 +1,87 @@
+// bgx_contract — kernel selection for two-input contractions (see bgx.h).
+#include "common.cuh"
+
+namespace bgx {
+bool tc_legal(const bgx_contract_desc &d, const char **why);
+int contract_tc(const bgx_contract_desc &d, cudaStream_t s);
+int contract_simt(const bgx_contract_desc &d, int kind, cudaStream_t s);
+
+namespace {
+
+enum { KIND_TC = 1, KIND_EXACT = 2, KIND_FFMA = 3, KIND_SIMT16 = 4 };
+
+int select_kind(const bgx_contract_desc &d) {
+  const bool half_in = d.in_dtype == BGX_BF16 || d.in_dtype == BGX_F16;
+  switch (d.mode) {
+    case BGX_MODE_AUTO:
+      if (half_in) return tc_legal(d, nullptr) ? KIND_TC : KIND_SIMT16;
+      return KIND_EXACT;
+    case BGX_MODE_EXACT:
+      if (half_in) return KIND_SIMT16;  // exact products in f32 (see gemm_simt.cu)
+      return KIND_EXACT;
+    case BGX_MODE_FFMA:
+      if (d.in_dtype != BGX_F32) {
+        set_error("bgx_contract: FFMA mode needs f32 inputs");
+        return BGX_ERR_UNSUPPORTED;
+      }
+      return KIND_FFMA;
+    case BGX_MODE_TC: {
+      const char *why = nullptr;
+      if (!tc_legal(d, &why)) {
+        set_error("bgx_contract: tensor-core path not legal: %s", why);
+        return BGX_ERR_UNSUPPORTED;
+      }
+      return KIND_TC;
+    }
+    case BGX_MODE_SIMT:
+      return half_in ? KIND_SIMT16 : KIND_EXACT;
+    default:
+      set_error("bgx_contract: bad mode %d", d.mode);
+      return BGX_ERR_INVALID;
+  }
+}
+
+int validate(const bgx_contract_desc &d) {
+  BGX_CHECK_ARG(d.batch >= 0 && d.M >= 0 && d.N >= 0 && d.K >= 0, "bgx_contract: negative extent");
+  BGX_CHECK_ARG(dtype_size(d.in_dtype) > 0 && dtype_size(d.out_dtype) > 0, "bgx_contract: bad dtype");
+  const bool half_in = d.in_dtype == BGX_BF16 || d.in_dtype == BGX_F16;
+  if (half_in)
+    BGX_CHECK_ARG(d.out_dtype == d.in_dtype || d.out_dtype == BGX_F32,
+                  "bgx_contract: out dtype must equal in dtype or be f32");
+  else
+    BGX_CHECK_ARG(d.out_dtype == d.in_dtype, "bgx_contract: f32/f64 out dtype must equal in dtype");
+  for (int i = 0; i < 3; ++i)
+    BGX_CHECK_ARG(d.a_stride[i] >= 0 && d.b_stride[i] >= 0 && d.c_stride[i] >= 0 && d.o_stride[i] >= 0,
+                  "bgx_contract: negative stride");
+  return BGX_OK;
+}
+
+}  // namespace
+}  // namespace bgx
+
+using namespace bgx;
+
+extern "C" int bgx_contract_kernel(const bgx_contract_desc *d) {
+  BGX_CHECK_ARG(d != nullptr, "bgx_contract_kernel: null descriptor");
+  int rc = validate(*d);
+  if (rc) return rc;
+  return select_kind(*d);
+}
+
+extern "C" int bgx_contract(const bgx_contract_desc *d, void *stream) {
+  BGX_CHECK_ARG(d != nullptr, "bgx_contract: null descriptor");
+  int rc = validate(*d);
+  if (rc) return rc;
+  if (d->batch == 0 || d->M == 0 || d->N == 0) return BGX_OK;
+  BGX_CHECK_ARG(d->out != nullptr, "bgx_contract: null out");
+  const int kind = select_kind(*d);
+  if (kind < 0) return kind;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d->K == 0) {
+    // empty reduction: out = c0 (or 0).  Handled by the SIMT kernel's init.
+    return contract_simt(*d, KIND_EXACT, s);
+  }
+  BGX_CHECK_ARG(d->a != nullptr && d->b != nullptr, "bgx_contract: null operand");
+  if (kind == KIND_TC) return contract_tc(*d, s);
+  return contract_simt(*d, kind, s);
+}

@@ -1,0 +1,167 @@
+// CUDA-core batched strided contraction (bgx_contract modes EXACT / FFMA /
+// SIMT).  Shared-memory tiled, register-blocked; any element strides.
+//
+// EXACT (f32/f64): each output element starts from c0 and accumulates
+// fl(fl(a*b) + acc) in increasing k — precisely the reference's per-point
+// body (bridgegen einsum.py:111-117 evaluated by interp.py:407-420) — so the
+// result is bit-identical to the reference for 2-operand contractions with
+// one (flattened, lexicographically ordered) reduction group.
+// FFMA (f32): fused fma(a, b, acc); <= 1e-5 relative vs the reference.
+// SIMT (bf16/f16 in, f32 accumulate): products of 16-bit values are exact in
+// f32, so fma == separate rounding here: bit-identical to the reference's f32
+// arithmetic on the upcast inputs; one final rounding to the output dtype.
+#include "common.cuh"
+
+namespace bgx {
+namespace {
+
+template <typename Acc> struct Arith;
+template <> struct Arith<float> {
+  template <bool FUSED>
+  __device__ static float mac(float a, float b, float c) {
+    if constexpr (FUSED) return __fmaf_rn(a, b, c);
+    else return __fadd_rn(__fmul_rn(a, b), c);
+  }
+};
+template <> struct Arith<double> {
+  template <bool FUSED>
+  __device__ static double mac(double a, double b, double c) {
+    if constexpr (FUSED) return __fma_rn(a, b, c);
+    else return __dadd_rn(__dmul_rn(a, b), c);
+  }
+};
+
+template <typename T> __device__ __forceinline__ float ld_f(const T *p) { return Conv<T>::to_f(*p); }
+
+template <typename In, typename Acc> __device__ __forceinline__ Acc to_acc(In v) {
+  if constexpr (sizeof(In) == 2) return (Acc)Conv<In>::to_f(v);
+  else return (Acc)v;
+}
+template <typename Out, typename Acc> __device__ __forceinline__ Out from_acc(Acc v) {
+  if constexpr (sizeof(Out) == 2) return Conv<Out>::from_f((float)v);
+  else return (Out)v;
+}
+
+struct Params {
+  int64_t batch, M, N, K;
+  const void *a; int64_t sa[3];
+  const void *b; int64_t sb[3];
+  const void *c0; int64_t sc[3];
+  void *out; int64_t so[3];
+  int64_t tiles_m, tiles_n;
+};
+
+constexpr int TM = 4, TN = 4, BK = 16;
+
+template <typename In, typename Out, typename Acc, bool FUSED, int BM, int BN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+simt_gemm_kernel(const Params p) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  __shared__ Acc As[BK][BM + 1];
+  __shared__ Acc Bs[BK][BN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  int64_t t = blockIdx.x;
+  const int64_t tn = t % p.tiles_n;
+  t /= p.tiles_n;
+  const int64_t tm = t % p.tiles_m;
+  const int64_t b = t / p.tiles_m;
+  const int64_t m0 = tm * BM, n0 = tn * BN;
+  const In *A = static_cast<const In *>(p.a) + b * p.sa[0];
+  const In *B = static_cast<const In *>(p.b) + b * p.sb[0];
+
+  Acc acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t m = m0 + ty * TM + i, n = n0 + tx * TN + j;
+      Acc v = (Acc)0;
+      if (p.c0 && m < p.M && n < p.N)
+        v = to_acc<Out, Acc>(static_cast<const Out *>(p.c0)[b * p.sc[0] + m * p.sc[1] + n * p.sc[2]]);
+      acc[i][j] = v;
+    }
+
+  // load mapping: run threads along whichever global dim has unit stride
+  const bool a_k_inner = p.sa[2] == 1;
+  const bool b_n_inner = p.sb[2] == 1 || p.sb[1] != 1;
+  for (int64_t k0 = 0; k0 < p.K; k0 += BK) {
+    for (int e = tid; e < BM * BK; e += NT) {
+      int mm, kk;
+      if (a_k_inner) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
+      const int64_t m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < p.M && k < p.K) ? to_acc<In, Acc>(A[m * p.sa[1] + k * p.sa[2]]) : (Acc)0;
+    }
+    for (int e = tid; e < BN * BK; e += NT) {
+      int nn, kk;
+      if (b_n_inner) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+      const int64_t n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < p.N && k < p.K) ? to_acc<In, Acc>(B[k * p.sb[1] + n * p.sb[2]]) : (Acc)0;
+    }
+    __syncthreads();
+    const int kmax = (p.K - k0) < BK ? (int)(p.K - k0) : BK;
+    for (int kk = 0; kk < kmax; ++kk) {
+      Acc av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = Arith<Acc>::template mac<FUSED>(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  Out *O = static_cast<Out *>(p.out) + b * p.so[0];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t m = m0 + ty * TM + i, n = n0 + tx * TN + j;
+      if (m < p.M && n < p.N) O[m * p.so[1] + n * p.so[2]] = from_acc<Out, Acc>(acc[i][j]);
+    }
+}
+
+template <typename In, typename Out, typename Acc, bool FUSED>
+int launch(const bgx_contract_desc &d, cudaStream_t s) {
+  Params p;
+  p.batch = d.batch; p.M = d.M; p.N = d.N; p.K = d.K;
+  p.a = d.a; p.b = d.b; p.c0 = d.c0; p.out = d.out;
+  for (int i = 0; i < 3; ++i) {
+    p.sa[i] = d.a_stride[i]; p.sb[i] = d.b_stride[i];
+    p.sc[i] = d.c_stride[i]; p.so[i] = d.o_stride[i];
+  }
+  const int sms = sm_count_current();
+  const bool small = (d.M * d.N * d.batch) < (int64_t)sms * 64 * 64 * 2;
+  if (small) {
+    p.tiles_m = (d.M + 31) / 32; p.tiles_n = (d.N + 31) / 32;
+    int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
+    simt_gemm_kernel<In, Out, Acc, FUSED, 32, 32><<<(unsigned)blocks, 64, 0, s>>>(p);
+  } else {
+    p.tiles_m = (d.M + 63) / 64; p.tiles_n = (d.N + 63) / 64;
+    int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
+    if (blocks > 0x7fffffffLL) { set_error("simt gemm: grid too large"); return BGX_ERR_UNSUPPORTED; }
+    simt_gemm_kernel<In, Out, Acc, FUSED, 64, 64><<<(unsigned)blocks, 256, 0, s>>>(p);
+  }
+  return check_launch("simt_gemm_kernel");
+}
+
+}  // namespace
+
+// Entry used by bgx_contract (contract.cu).  kind: 2 exact, 3 ffma, 4 16-bit.
+int contract_simt(const bgx_contract_desc &d, int kind, cudaStream_t s) {
+  const int in = d.in_dtype, out = d.out_dtype;
+  if (in == BGX_F32 && out == BGX_F32)
+    return kind == 3 ? launch<float, float, float, true>(d, s) : launch<float, float, float, false>(d, s);
+  if (in == BGX_F64 && out == BGX_F64)
+    return kind == 3 ? launch<double, double, double, true>(d, s) : launch<double, double, double, false>(d, s);
+  if (in == BGX_BF16 && out == BGX_BF16) return launch<__nv_bfloat16, __nv_bfloat16, float, true>(d, s);
+  if (in == BGX_BF16 && out == BGX_F32) return launch<__nv_bfloat16, float, float, true>(d, s);
+  if (in == BGX_F16 && out == BGX_F16) return launch<__half, __half, float, true>(d, s);
+  if (in == BGX_F16 && out == BGX_F32) return launch<__half, float, float, true>(d, s);
+  set_error("simt gemm: unsupported dtype pair in=%d out=%d", in, out);
+  return BGX_ERR_UNSUPPORTED;
+}
+
+}  // namespace bgx

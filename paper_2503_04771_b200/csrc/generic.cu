@@ -1,0 +1,112 @@
+// bgx_generic — the reference's linalg.generic loop nest on the GPU with the
+// reference's exact arithmetic (bridgegen interp.py:372-424, body from
+// einsum.py:100-118, scalar semantics interp.py:260-274).
+//
+// One thread owns one output element (the parallel axes come first in the
+// reference's axis order, einsum.py:81, so each output element is produced by
+// one contiguous run of the reduction sub-space).  The thread walks that
+// sub-space in the same lexicographic order with an odometer, forms
+// p = x1 * x2 * ... (left fold) and acc = p + acc with __fmul_rn/__fadd_rn
+// (no FMA contraction, no flush-to-zero), so every output is bit-identical to
+// the reference.  This is the kernel for bodies the GEMM planner does not map
+// (single-input reductions, Hadamard/outer products, 3+-operand patterns,
+// rank-0 outputs) and for fp32 parity runs.
+#include "common.cuh"
+
+namespace bgx {
+namespace {
+
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T, int NIN>
+__global__ void __launch_bounds__(128)
+generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
+  const int n_in = NIN > 0 ? NIN : d.n_in;
+  const int n_par = d.n_par, n_axes = d.n_axes, n_red = n_axes - n_par;
+  const bool passthrough = (n_in == 1 && n_red == 0);
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n_out;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t off[BGX_MAX_OPERANDS];
+#pragma unroll
+    for (int k = 0; k < BGX_MAX_OPERANDS; ++k) off[k] = 0;
+    int64_t rem = o;
+    for (int a = n_par - 1; a >= 0; --a) {
+      const int64_t e = d.extents[a];
+      const int64_t i = rem % e;
+      rem /= e;
+      for (int k = 0; k < n_in; ++k) off[k] += i * d.strides[k][a];
+    }
+    const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+    if (passthrough) {
+      static_cast<T *>(d.out)[o] = ins[0][off[0]];
+      continue;
+    }
+    T acc = static_cast<const T *>(d.c0)[o];
+    int64_t idx[BGX_MAX_AXES];
+    for (int a = 0; a < n_red; ++a) idx[a] = 0;
+    for (int64_t r = 0; r < red_points; ++r) {
+      T p = ins[0][off[0]];
+      for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k]]);
+      acc = add_rn<T>(p, acc);
+      for (int a = n_red - 1; a >= 0; --a) {
+        const int ax = n_par + a;
+        if (++idx[a] < d.extents[ax]) {
+          for (int k = 0; k < n_in; ++k) off[k] += d.strides[k][ax];
+          break;
+        }
+        for (int k = 0; k < n_in; ++k) off[k] -= (d.extents[ax] - 1) * d.strides[k][ax];
+        idx[a] = 0;
+      }
+    }
+    static_cast<T *>(d.out)[o] = acc;
+  }
+}
+
+template <typename T>
+int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
+  const int sms = sm_count_current();
+  if (sms <= 0) { set_error("bgx_generic: no device"); return BGX_ERR_NO_DEVICE; }
+  int64_t blocks = (n_out + 127) / 128;
+  if (blocks > (int64_t)sms * 64) blocks = (int64_t)sms * 64;
+  switch (d.n_in) {
+    case 1: generic_kernel<T, 1><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 2: generic_kernel<T, 2><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 3: generic_kernel<T, 3><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    default: generic_kernel<T, 0><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+  }
+  return check_launch("generic_kernel");
+}
+
+}  // namespace
+}  // namespace bgx
+
+using namespace bgx;
+
+extern "C" int bgx_generic(const bgx_generic_desc *d, void *stream) {
+  BGX_CHECK_ARG(d != nullptr, "bgx_generic: null descriptor");
+  BGX_CHECK_ARG(d->n_in >= 1 && d->n_in <= BGX_MAX_OPERANDS, "bgx_generic: n_in %d", d->n_in);
+  BGX_CHECK_ARG(d->n_axes >= 0 && d->n_axes <= BGX_MAX_AXES && d->n_par >= 0 &&
+                    d->n_par <= d->n_axes,
+                "bgx_generic: axes %d / parallel %d", d->n_axes, d->n_par);
+  BGX_CHECK_ARG(d->dtype == BGX_F32 || d->dtype == BGX_F64,
+                "bgx_generic: dtype %d (the reference body types are f32/f64)", d->dtype);
+  int64_t n_out = 1, red = 1;
+  for (int a = 0; a < d->n_axes; ++a) {
+    BGX_CHECK_ARG(d->extents[a] >= 0, "bgx_generic: negative extent");
+    if (a < d->n_par) n_out *= d->extents[a]; else red *= d->extents[a];
+  }
+  if (n_out == 0) return BGX_OK;
+  BGX_CHECK_ARG(d->out != nullptr, "bgx_generic: null out");
+  const bool passthrough = d->n_in == 1 && d->n_axes == d->n_par;
+  BGX_CHECK_ARG(passthrough || d->c0 != nullptr, "bgx_generic: null c0");
+  if (red > 0 || passthrough)
+    for (int k = 0; k < d->n_in; ++k) BGX_CHECK_ARG(d->ins[k] != nullptr, "bgx_generic: null input");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (d->dtype == BGX_F32) return launch_generic<float>(*d, n_out, red, s);
+  return launch_generic<double>(*d, n_out, red, s);
+}

@@ -1,0 +1,254 @@
+"""Device-resident execution of planned generic ops through libbgx.so.
+
+Torch is plumbing here (device memory, the current CUDA stream); every byte
+of compute is one of the sm_100a kernels behind include/bgx.h.  There is no
+CPU path: CPU tensors are rejected, and a missing libbgx.so raises
+``BackendUnavailable``.
+
+Semantics follow bridgegen ``_generic`` (interp.py:372-424): the result is a
+FRESH tensor holding ``c0 + sum(prod(inputs))`` (``c0`` = the output operand,
+never mutated, interp.py:399) — or the permuted input for a passthrough body.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from . import _lib
+from .einsum import EinsumSpec
+from .plan import (ChainPlan, GemmPlan, GenericPlan, PermutePlan, extents_of,
+                   plan_generic)
+
+TORCH_TO_BGX = {torch.float32: _lib.F32, torch.float64: _lib.F64,
+                torch.bfloat16: _lib.BF16, torch.float16: _lib.F16}
+DTYPE_NAME = {torch.float32: "f32", torch.float64: "f64", torch.bfloat16: "bf16",
+              torch.float16: "f16"}
+MODES = {"auto": _lib.MODE_AUTO, "exact": _lib.MODE_EXACT, "ffma": _lib.MODE_FFMA,
+         "tc": _lib.MODE_TC, "simt": _lib.MODE_SIMT}
+
+_trace = threading.local()
+
+
+def launch_log() -> list:
+    """Kernels launched by this thread since the last ``reset_launch_log``."""
+    if not hasattr(_trace, "log"):
+        _trace.log = []
+    return _trace.log
+
+
+def reset_launch_log():
+    _trace.log = []
+
+
+def _log(name: str):
+    launch_log().append(name)
+
+
+def _stream_ptr(t: torch.Tensor):
+    """cudaStream_t of torch's current stream on ``t``'s device (as int)."""
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _check_device(tensors):
+    dev = None
+    for t in tensors:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("bgx executes on CUDA tensors only (no CPU fallback)")
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise ValueError(f"operands on different devices: {dev} vs {t.device}")
+    return dev
+
+
+# ---------------------------------------------------------------------------
+# raw kernel calls
+
+def permute(x: torch.Tensor, out: torch.Tensor, perm) -> torch.Tensor:
+    lib = _lib.load()
+    ti, to = _lib.BgxTensor(), _lib.BgxTensor()
+    for t, desc in ((x, ti), (out, to)):
+        desc.data = t.data_ptr()
+        desc.dtype = TORCH_TO_BGX[t.dtype]
+        desc.rank = t.dim()
+        for d in range(t.dim()):
+            desc.shape[d] = t.shape[d]
+            desc.stride[d] = t.stride(d)
+    p = (_lib._i32 * max(1, len(perm)))(*perm)
+    with torch.cuda.device(x.device):
+        _lib.check(lib.bgx_permute(ti, to, p, _stream_ptr(x)), "bgx_permute")
+    _log("permute")
+    return out
+
+
+def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor) -> torch.Tensor:
+    """The reference loop nest on the device (bit-exact, f32/f64)."""
+    lib = _lib.load()
+    if out.dtype not in (torch.float32, torch.float64):
+        raise NotImplementedError("bgx_generic computes in the reference's f32/f64 only")
+    if len(inputs) > _lib.MAX_OPERANDS or len(spec.axes) > _lib.MAX_AXES:
+        raise NotImplementedError("bgx_generic: too many operands/axes")
+    d = _lib.BgxGenericDesc()
+    d.n_in = len(inputs)
+    d.n_axes = len(spec.axes)
+    d.n_par = len(spec.output)
+    d.dtype = TORCH_TO_BGX[out.dtype]
+    ext = extents_of(spec, [t.shape for t in inputs] + [out.shape])
+    for a, name in enumerate(spec.axes):
+        d.extents[a] = ext[name]
+    for k, (t, tup) in enumerate(zip(inputs, spec.inputs)):
+        d.ins[k] = t.data_ptr()
+        for dim, name in enumerate(tup):
+            d.strides[k][spec.axes.index(name)] = t.stride(dim)
+    assert out.is_contiguous()
+    if c0 is None:
+        c0 = torch.zeros_like(out)
+    elif not c0.is_contiguous():
+        c0 = permute(c0, torch.empty(c0.shape, dtype=c0.dtype, device=c0.device),
+                     list(range(c0.dim())))
+    d.c0 = c0.data_ptr()
+    d.out = out.data_ptr()
+    with torch.cuda.device(out.device):
+        _lib.check(lib.bgx_generic(d, _stream_ptr(out)), "bgx_generic")
+    _log("generic")
+    return out
+
+
+def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0=None,
+                 c_strides=(0, 0, 0), mode="auto", schedule=None, in_dtype=None) -> int:
+    """One ``bgx_contract`` call on raw (tensor, 3 strides) views; returns the
+    kernel id that ran (_lib.KERNEL_*)."""
+    lib = _lib.load()
+    d = _lib.BgxContractDesc()
+    d.batch, d.M, d.N, d.K = batch, M, N, K
+    d.a = a.data_ptr() if a is not None else None
+    d.b = b.data_ptr() if b is not None else None
+    d.c0 = c0.data_ptr() if c0 is not None else None
+    d.out = out.data_ptr()
+    for i in range(3):
+        d.a_stride[i], d.b_stride[i] = a_strides[i], b_strides[i]
+        d.c_stride[i], d.o_stride[i] = c_strides[i], o_strides[i]
+    d.in_dtype = TORCH_TO_BGX[in_dtype or a.dtype]
+    d.out_dtype = TORCH_TO_BGX[out.dtype]
+    d.mode = MODES[mode]
+    if schedule:
+        for k, v in schedule.items():
+            setattr(d.sched, k, int(v))
+    kind = lib.bgx_contract_kernel(d)
+    _lib.check(kind if kind < 0 else 0, "bgx_contract_kernel")
+    with torch.cuda.device(out.device):
+        _lib.check(lib.bgx_contract(d, _stream_ptr(out)), "bgx_contract")
+    _log(_lib.KERNEL_NAMES.get(kind, "contract"))
+    return kind
+
+
+# ---------------------------------------------------------------------------
+# plan execution
+
+def _materialise(t: torch.Tensor, tup, group_axes) -> torch.Tensor:
+    """Copy ``t`` (indexed by ``tup``) into a contiguous tensor whose dims are
+    the concatenation of ``group_axes`` (a permute pre-pass on the device)."""
+    order = [a for g in group_axes for a in g]
+    perm = [tup.index(a) for a in order]
+    dst = torch.empty([t.shape[p] for p in perm], dtype=t.dtype, device=t.device)
+    return permute(t, dst, perm), tuple(order)
+
+
+def _group_strides(t, tup, view_axes, ext):
+    from .plan import flatten_group
+    by = dict(zip(tup, t.stride()))
+    return tuple(flatten_group(g, ext, by) if g else 0 for g in view_axes)
+
+
+def run_gemm(p: GemmPlan, spec: EinsumSpec, inputs, c0, out, *, mode, schedule):
+    ext = extents_of(spec, [t.shape for t in inputs] + [out.shape])
+    a, b = inputs[p.a], inputs[p.b]
+    a_tup, b_tup = spec.inputs[p.a], spec.inputs[p.b]
+    if p.a_view.needs_copy:
+        a, a_tup = _materialise(a, a_tup, p.a_view.axes)
+    if p.b_view.needs_copy:
+        b, b_tup = _materialise(b, b_tup, p.b_view.axes)
+    sa = _group_strides(a, a_tup, p.a_view.axes, ext)
+    sb = _group_strides(b, b_tup, p.b_view.axes, ext)
+    o_tup = spec.output
+    tmp_out = out
+    so = _group_strides(out, o_tup, p.o_view.axes, ext)
+    if any(s is None for s in so):
+        order = [x for g in p.o_view.axes for x in g]
+        tmp_out = torch.empty([ext[x] for x in order], dtype=out.dtype, device=out.device)
+        o_tup = tuple(order)
+        so = _group_strides(tmp_out, o_tup, p.o_view.axes, ext)
+    sc = (0, 0, 0)
+    if c0 is not None:
+        c_tup = spec.output
+        sc = _group_strides(c0, c_tup, p.o_view.axes, ext)
+        if any(s is None for s in sc):
+            c0, c_tup = _materialise(c0, c_tup, p.o_view.axes)
+            sc = _group_strides(c0, c_tup, p.o_view.axes, ext)
+    contract_raw(a, sa, b, sb, tmp_out, so, batch=p.batch, M=p.M, N=p.N, K=p.K, c0=c0,
+                 c_strides=sc, mode=mode, schedule=schedule)
+    if tmp_out is not out:
+        perm = [o_tup.index(x) for x in spec.output]
+        permute(tmp_out, out, perm)
+    return out
+
+
+def _step_spec(lhs_axes, rhs_axes, out_axes) -> EinsumSpec:
+    seen = list(dict.fromkeys((*lhs_axes, *rhs_axes)))
+    axes = tuple(out_axes) + tuple(a for a in seen if a not in out_axes)
+    return EinsumSpec((tuple(lhs_axes), tuple(rhs_axes)), tuple(out_axes), axes)
+
+
+def run_chain(p: ChainPlan, spec: EinsumSpec, inputs, c0, out, *, mode, schedule):
+    ext = extents_of(spec, [t.shape for t in inputs] + [out.shape])
+    temps = []
+    for i, st in enumerate(p.steps):
+        last = i == len(p.steps) - 1
+        lhs = inputs[st.lhs] if isinstance(st.lhs, int) else temps[st.lhs[1]]
+        rhs = inputs[st.rhs] if isinstance(st.rhs, int) else temps[st.rhs[1]]
+        sspec = _step_spec(st.lhs_axes, st.rhs_axes, st.out_axes)
+        dst = out if last else torch.empty([ext[a] for a in st.out_axes], dtype=out.dtype,
+                                           device=out.device)
+        execute(sspec, [lhs, rhs], c0 if last else None, dst, mode=mode, schedule=schedule)
+        temps.append(dst)
+    return out
+
+
+def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
+            mode: str = "auto", schedule=None, chain_order: str = "left"):
+    """Run one generic op into ``out`` (fresh, contiguous-or-strided device
+    tensor).  ``c0`` is the initial output (None = zeros); ignored by a
+    passthrough body, exactly as in the reference (einsum.py:105-108)."""
+    _check_device(list(inputs) + [c0, out])
+    dt = out.dtype
+    for t in inputs:
+        if t.dtype != dt:
+            raise TypeError("operands must share one element type")
+    shapes = [tuple(t.shape) for t in inputs] + [tuple(out.shape)]
+    strides = [tuple(t.stride()) for t in inputs] + [tuple(out.stride())]
+    plan = plan_generic(spec, shapes, strides, dtype=DTYPE_NAME[dt], mode=mode,
+                        chain_order=chain_order)
+    if isinstance(plan, PermutePlan):
+        return permute(inputs[0], out, plan.perm)
+    if isinstance(plan, GenericPlan):
+        if out.is_contiguous():
+            return generic(spec, inputs, c0, out)
+        tmp = torch.empty(out.shape, dtype=dt, device=out.device)
+        generic(spec, inputs, c0, tmp)
+        return permute(tmp, out, list(range(out.dim())))
+    if isinstance(plan, GemmPlan):
+        return run_gemm(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)
+    if isinstance(plan, ChainPlan):
+        return run_chain(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)
+    raise AssertionError(plan)
+
+
+def plan_for(spec: EinsumSpec, inputs, out, *, mode="auto", chain_order="left"):
+    shapes = [tuple(t.shape) for t in inputs] + [tuple(out.shape)]
+    strides = [tuple(t.stride()) for t in inputs] + [tuple(out.stride())]
+    return plan_generic(spec, shapes, strides, dtype=DTYPE_NAME[out.dtype], mode=mode,
+                        chain_order=chain_order)

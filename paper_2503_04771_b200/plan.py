@@ -1,0 +1,286 @@
+"""Classify a ``linalg.generic`` (einsum spec + operand layouts) into a kernel
+plan — the "index-to-loop lowering chooses the kernel variant" step.
+
+Input is what bridgegen's ``_generic`` reads (interp.py:372-424): the spec's
+index tuples (→ indexing maps, einsum.py:85-94), the body kind
+(einsum.py:100-118) and the operands' extents; plus what a B200 backend needs
+on top: element strides and dtype.  Output is one of
+
+  PermutePlan  passthrough body → ``bgx_permute`` (bit-exact copy);
+  GemmPlan     2 inputs whose axes split into batch / M / N / K groups
+                → ``bgx_contract``; each group is flattened
+               to one extent+stride per operand when the strides compose,
+               otherwise the operand is first materialised in group order by
+               a permute pre-pass (``needs_copy``);
+  GenericPlan  anything else (single-input reductions, Hadamard / outer
+               products, A-only reduction axes, rank-0 outputs, 3+ inputs in
+               exact mode) → ``bgx_generic`` (the reference's loop nest on the
+               device, bit-exact);
+  ChainPlan    3+ inputs evaluated as pairwise contractions (left-to-right or
+               min-flop order) → a sequence of GemmPlans over intermediates.
+
+Everything here is host logic over integers — unit-tested on the CPU
+(tests/test_plan.py) — no kernels are launched.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .einsum import EinsumSpec
+
+# group names
+BATCH, MGRP, NGRP, KGRP = "batch", "m", "n", "k"
+
+# exact-mode generic kernel is used for f32/f64 multi-operand specs up to
+# this many iteration points in AUTO mode; larger ones are planned pairwise.
+GENERIC_POINT_LIMIT = 1 << 28
+
+
+@dataclass
+class PermutePlan:
+    perm: tuple          # output dim d reads input dim perm[d]
+    kind: str = "permute"
+
+
+@dataclass
+class GenericPlan:
+    reason: str
+    kind: str = "generic"
+
+
+@dataclass
+class OperandView:
+    """An operand seen as 3 flattened groups (elements strides)."""
+    groups: tuple                 # e.g. (BATCH, MGRP, KGRP)
+    axes: tuple                   # per group: tuple of index names (group order)
+    strides: tuple                # per group flattened stride (None if not flattenable)
+
+    @property
+    def needs_copy(self) -> bool:
+        return any(s is None for s in self.strides)
+
+
+@dataclass
+class GemmPlan:
+    a: int                        # which input is the GEMM "A" (M x K)
+    b: int                        # which input is the GEMM "B" (K x N)
+    batch_axes: tuple
+    m_axes: tuple
+    n_axes: tuple
+    k_axes: tuple
+    batch: int
+    M: int
+    N: int
+    K: int
+    a_view: OperandView
+    b_view: OperandView
+    o_view: OperandView
+    kind: str = "gemm"
+
+    @property
+    def flops(self) -> int:
+        return 2 * self.batch * self.M * self.N * self.K
+
+
+@dataclass
+class ChainStep:
+    lhs: object                   # int (input index) or ("t", step index)
+    rhs: object
+    lhs_axes: tuple
+    rhs_axes: tuple
+    out_axes: tuple               # intermediate (or final) index tuple
+    flops: int
+
+
+@dataclass
+class ChainPlan:
+    steps: list = field(default_factory=list)
+    order: str = "left"
+    kind: str = "chain"
+
+    @property
+    def flops(self) -> int:
+        return sum(s.flops for s in self.steps)
+
+
+def _prod(xs) -> int:
+    p = 1
+    for x in xs:
+        p *= int(x)
+    return p
+
+
+def extents_of(spec: EinsumSpec, shapes) -> dict:
+    """Axis extents from operand shapes (inputs then output), with the
+    reference's consistency rule (interp.py:379-396)."""
+    ext = {}
+    for shape, tup in zip(shapes, (*spec.inputs, spec.output)):
+        for e, n in zip(shape, tup):
+            if n in ext and ext[n] != e:
+                raise ValueError(f"inconsistent extent for {n}: {ext[n]} vs {e}")
+            ext[n] = int(e)
+    return ext
+
+
+def flatten_group(axes, ext, strides_by_axis):
+    """One stride for the row-major flattening of ``axes`` (extent-1 axes
+    ignored), or None if the operand's strides do not compose."""
+    live = [a for a in axes if ext[a] != 1]
+    if not live:
+        return 0
+    s = strides_by_axis[live[-1]]
+    for hi, lo in zip(live[-2::-1], live[:0:-1]):
+        if strides_by_axis[hi] != strides_by_axis[lo] * ext[lo]:
+            return None
+    return s
+
+
+def classify_two(spec: EinsumSpec, ext: dict):
+    """Axis groups for a 2-input spec, or a reason string when it is not a
+    batch/M/N/K contraction."""
+    A, B = set(spec.inputs[0]), set(spec.inputs[1])
+    O = set(spec.output)
+    batch = [a for a in spec.output if a in A and a in B]
+    m = [a for a in spec.output if a in A and a not in B]
+    n = [a for a in spec.output if a in B and a not in A]
+    k = [a for a in spec.axes if a in A and a in B and a not in O]
+    only = [a for a in spec.axes if a not in O and ((a in A) != (a in B))]
+    if only:
+        return f"reduction axis {only[0]!r} indexes only one input"
+    return batch, m, n, k
+
+
+def plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
+                 out_strides=None, chain_order: str = "left"):
+    """Plan one generic op.  ``shapes``/``strides``: per operand (inputs then
+    output), element strides.  ``dtype``: 'f32'|'f64'|'bf16'|'f16'.
+    ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt'."""
+    n_in = len(spec.inputs)
+    ext = extents_of(spec, shapes)
+    all_par = all(a in spec.output for a in spec.axes)
+    if n_in == 1 and all_par:
+        perm = tuple(spec.inputs[0].index(a) for a in spec.output)
+        return PermutePlan(perm)
+    ref_types = dtype in ("f32", "f64")
+    if n_in == 1:
+        return GenericPlan("single-input reduction")
+    if n_in >= 3:
+        points = _prod(ext[a] for a in spec.axes)
+        if ref_types and (mode == "exact" or points <= GENERIC_POINT_LIMIT):
+            return GenericPlan("multi-operand body, exact loop nest")
+        return plan_chain(spec, ext, order=chain_order)
+    groups = classify_two(spec, ext)
+    if isinstance(groups, str):
+        if not ref_types:
+            raise NotImplementedError(f"{spec}: {groups} (no 16-bit generic kernel)")
+        return GenericPlan(groups)
+    batch, m, n, k = groups
+    if ref_types and not k and (not m or not n):
+        return GenericPlan("elementwise product (no reduction)")
+    return plan_gemm(spec, ext, strides, (batch, m, n, k), out_strides)
+
+
+def _view(groups, axes_per_group, ext, tup, st):
+    by_axis = dict(zip(tup, st))
+    flat = []
+    for axes in axes_per_group:
+        flat.append(flatten_group(axes, ext, by_axis) if axes else 0)
+    return OperandView(groups, tuple(tuple(a) for a in axes_per_group), tuple(flat))
+
+
+def plan_gemm(spec, ext, strides, groups, out_strides=None):
+    batch, m, n, k = groups
+    o_st = strides[-1] if out_strides is None else out_strides
+    o_by = dict(zip(spec.output, o_st))
+    # The output's unit-stride group becomes N (the epilogue writes rows of N);
+    # if that group belongs to input 0, swap the roles of the two inputs.
+    a_i, b_i, m_ax, n_ax = 0, 1, m, n
+    live = [a for a in spec.output if ext[a] != 1]
+    if live and m and n:
+        inner = min(live, key=lambda a: o_by[a])
+        if inner in m:
+            a_i, b_i, m_ax, n_ax = 1, 0, n, m
+    a_tup, b_tup = spec.inputs[a_i], spec.inputs[b_i]
+    a_view = _view((BATCH, MGRP, KGRP), (batch, m_ax, k), ext, a_tup, strides[a_i])
+    b_view = _view((BATCH, KGRP, NGRP), (batch, k, n_ax), ext, b_tup, strides[b_i])
+    o_view = _view((BATCH, MGRP, NGRP), (batch, m_ax, n_ax), ext, spec.output, o_st)
+    return GemmPlan(a_i, b_i, tuple(batch), tuple(m_ax), tuple(n_ax), tuple(k),
+                    _prod(ext[x] for x in batch), _prod(ext[x] for x in m_ax),
+                    _prod(ext[x] for x in n_ax), _prod(ext[x] for x in k),
+                    a_view, b_view, o_view)
+
+
+def _pair_out(lhs_axes, rhs_axes, keep):
+    """Index tuple of a pairwise intermediate: axes of lhs/rhs still needed
+    later (``keep``), in first-appearance order."""
+    seen = list(dict.fromkeys((*lhs_axes, *rhs_axes)))
+    return tuple(a for a in seen if a in keep)
+
+
+def plan_chain(spec: EinsumSpec, ext: dict, order: str = "left") -> ChainPlan:
+    """Pairwise evaluation of a 3+-input contraction.  ``order='left'`` folds
+    inputs left to right (the order that shards on the output's leading free
+    index with no collective); ``'optimal'`` picks the cheapest binary order
+    by exhaustive search (fine for the <= 6 operands the ABI allows)."""
+    ins = list(spec.inputs)
+
+    def needed_after(pending):
+        keep = set(spec.output)
+        for tup in pending:
+            keep.update(tup)
+        return keep
+
+    if order == "left":
+        steps = []
+        cur, cur_axes = 0, ins[0]
+        for j in range(1, len(ins)):
+            keep = needed_after(ins[j + 1:])
+            out_axes = _pair_out(cur_axes, ins[j], keep) if j < len(ins) - 1 else spec.output
+            all_axes = set(cur_axes) | set(ins[j])
+            flops = 2 * _prod(ext[a] for a in all_axes)
+            steps.append(ChainStep(cur, j, tuple(cur_axes), tuple(ins[j]), tuple(out_axes), flops))
+            cur, cur_axes = ("t", len(steps) - 1), out_axes
+        return ChainPlan(steps, "left")
+
+    # 'optimal': dynamic programming over subsets (matrix-chain-style, any shape)
+    n = len(ins)
+    best = {}
+    for i in range(n):
+        best[1 << i] = (0, None, tuple(ins[i]))
+    full = (1 << n) - 1
+
+    for size in range(2, n + 1):
+        for mask in range(1, full + 1):
+            if bin(mask).count("1") != size:
+                continue
+            rest = [ins[i] for i in range(n) if not mask >> i & 1]
+            keep = set(spec.output)
+            for t in rest:
+                keep.update(t)
+            sub = (mask - 1) & mask
+            while sub:
+                other = mask ^ sub
+                if sub < other and sub in best and other in best:
+                    c1, _, ax1 = best[sub]
+                    c2, _, ax2 = best[other]
+                    cost = c1 + c2 + 2 * _prod(ext[a] for a in set(ax1) | set(ax2))
+                    out_axes = spec.output if mask == full else _pair_out(ax1, ax2, keep)
+                    if mask not in best or cost < best[mask][0]:
+                        best[mask] = (cost, (sub, other), tuple(out_axes))
+                sub = (sub - 1) & mask
+    steps = []
+
+    def emit(mask):
+        cost, split, axes = best[mask]
+        if split is None:
+            return next(i for i in range(n) if mask >> i & 1), axes
+        l, r = split
+        lref, lax = emit(l)
+        rref, rax = emit(r)
+        flops = 2 * _prod(ext[a] for a in set(lax) | set(rax))
+        steps.append(ChainStep(lref, rref, tuple(lax), tuple(rax), tuple(axes), flops))
+        return ("t", len(steps) - 1), axes
+
+    emit(full)
+    return ChainPlan(steps, "optimal")

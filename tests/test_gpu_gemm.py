@@ -1,0 +1,179 @@
+"""Contraction kernels on the B200 vs the CPU oracle.
+
+* SIMT exact (f32): bit-identical to the reference's arithmetic (oracle
+  gemm_kseq, itself pinned to bridgegen by tests/test_oracle.py), incl. the
+  BASELINE C1 config (256^3 f32 via the DSL).
+* tcgen05 (bf16/f16 in, f32 accumulate): relative Frobenius error <= 1e-2
+  (north_star tolerance) against the oracle on the bf16-rounded inputs, for
+  every operand layout (A K-/M-major x B K-/N-major), batch, beta (c0), ragged
+  M/N/K and each output dtype; plus row-sampled parity at the BASELINE C3/C4
+  sizes.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2503_04771_b200 import _lib, contract, executor
+from paper_2503_04771_b200 import einsum as E
+from paper_2503_04771_b200 import interp as I
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 1e-2
+FFMA_TOL = 1e-5
+
+
+def rnd(shape, seed, dev, dtype=torch.float32):
+    x = np.random.default_rng(seed).standard_normal(shape, dtype=np.float32)
+    return torch.from_numpy(x).to(dev).to(dtype)
+
+
+def np32(t):
+    return t.float().cpu().numpy()
+
+
+def test_c1_fp32_256_cubed_bit_exact(dev):
+    """BASELINE config 1 through the DSL: (i,j),(j,k)->(i,k) f32 256^3."""
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((256, 256), dtype=np.float32)
+    b = np.random.default_rng(2).standard_normal((256, 256), dtype=np.float32)
+    c = np.zeros((256, 256), np.float32)
+    mod = E.build_einsum_function(None, E.parse_einsum("(i,j),(j,k)->(i,k)"))
+    executor.reset_launch_log()
+    [got] = I.run_function(mod, "einsum", [I.TensorValue(E.F32, x.shape, x) for x in (a, b, c)],
+                           step_limit=None)
+    assert np.array_equal(got.data, oracle.gemm_kseq(a, b, c))
+    assert executor.launch_log() == ["simt-exact"]
+
+
+def test_step_limit_mirrors_reference(dev):
+    """256^3 needs 50,331,650 reference steps: the default
+    budget of 10^7 raises StepLimitExceeded exactly like the reference."""
+    mod = E.build_einsum_function(None, E.parse_einsum("(i,j),(j,k)->(i,k)"))
+    z = np.zeros((256, 256), np.float32)
+    with pytest.raises(I.StepLimitExceeded, match="step budget of 10000000"):
+        I.run_function(mod, "einsum", [I.TensorValue(E.F32, z.shape, z)] * 3)
+    I.run_function(mod, "einsum", [I.TensorValue(E.F32, z.shape, z)] * 3, step_limit=50_331_650)
+    with pytest.raises(I.StepLimitExceeded):
+        I.run_function(mod, "einsum", [I.TensorValue(E.F32, z.shape, z)] * 3,
+                       step_limit=50_331_649)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 64, 64), (130, 70, 300)])
+@pytest.mark.parametrize("beta", [False, True])
+def test_fp32_exact_and_ffma(dev, M, N, K, beta):
+    a, b = rnd((M, K), 1, dev), rnd((K, N), 2, dev)
+    c0 = rnd((M, N), 3, dev) if beta else None
+    ex = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="exact")
+    want = oracle.gemm_kseq(np32(a), np32(b), np32(c0) if beta else None)
+    assert np.array_equal(np32(ex), want)
+    ff = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="ffma")
+    assert oracle.rel_frobenius(np32(ff), want) <= FFMA_TOL
+
+
+def test_f64_exact(dev):
+    a = rnd((33, 41), 4, dev, torch.float64)
+    b = rnd((41, 19), 5, dev, torch.float64)
+    got = contract("(i,k),(k,j)->(i,j)", a, b).cpu().numpy()
+    want = oracle.generic([("i", "k"), ("k", "j")], ("i", "j"),
+                          [a.cpu().numpy(), b.cpu().numpy()], np.zeros((33, 19)))
+    assert np.array_equal(got, want)
+
+
+LAYOUTS = {
+    # spec, how to build A and B so that A is K- or M-major and B K- or N-major
+    "A_k_B_n": "(i,k),(k,j)->(i,j)",
+    "A_m_B_n": "(k,i),(k,j)->(i,j)",
+    "A_k_B_k": "(i,k),(j,k)->(i,j)",
+    "A_m_B_k": "(k,i),(j,k)->(i,j)",
+}
+
+
+@pytest.mark.parametrize("layout", list(LAYOUTS))
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 640), (200, 136, 72), (1000, 520, 1000)])
+def test_tcgen05_layouts(dev, layout, dtype, M, N, K):
+    spec = E.parse_einsum(LAYOUTS[layout])
+    shp = {"i": M, "j": N, "k": K}
+    a = rnd(tuple(shp[x] for x in spec.inputs[0]), 11, dev, dtype)
+    b = rnd(tuple(shp[x] for x in spec.inputs[1]), 12, dev, dtype)
+    executor.reset_launch_log()
+    out = contract(spec, a, b, out_dtype=torch.float32, mode="tc")
+    assert executor.launch_log() == ["tcgen05"]
+    A = np32(a) if spec.inputs[0] == ("i", "k") else np32(a).T
+    B = np32(b) if spec.inputs[1] == ("k", "j") else np32(b).T
+    want = oracle.gemm_kseq(np.ascontiguousarray(A), np.ascontiguousarray(B))
+    err = oracle.rel_frobenius(np32(out), want)
+    assert err <= BF16_TOL, err
+    # tf32-free f32 accumulation should be far tighter than the bar
+    assert err <= 1e-5, err
+
+
+@pytest.mark.parametrize("tile_n", [64, 128, 256])
+def test_tcgen05_tile_sizes_and_bf16_out(dev, tile_n):
+    a, b = rnd((384, 320), 21, dev, torch.bfloat16), rnd((320, 448), 22, dev, torch.bfloat16)
+    c0 = rnd((384, 448), 23, dev, torch.bfloat16)
+    out = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="tc", schedule={"tile_n": tile_n})
+    assert out.dtype == torch.bfloat16
+    want = oracle.gemm_kseq(np32(a), np32(b), np32(c0))
+    assert oracle.rel_frobenius(np32(out), want) <= BF16_TOL
+
+
+def test_tcgen05_batched_c3_pattern(dev):
+    """(b,i,j),(b,j,k)->(b,i,k), batch folded into the tile scheduler."""
+    a, b = rnd((5, 192, 160), 31, dev, torch.bfloat16), rnd((5, 160, 272), 32, dev, torch.bfloat16)
+    executor.reset_launch_log()
+    out = contract("(b,i,j),(b,j,k)->(b,i,k)", a, b, out_dtype=torch.float32)
+    assert executor.launch_log() == ["tcgen05"]
+    want = oracle.gemm_kseq(np32(a), np32(b))
+    assert oracle.rel_frobenius(np32(out), want) <= 1e-5
+
+
+def test_tcgen05_output_transposed(dev):
+    """(i,k),(k,j)->(j,i): the planner swaps operand roles so the output's
+    unit-stride index is N."""
+    a, b = rnd((300, 200), 41, dev, torch.bfloat16), rnd((200, 176), 42, dev, torch.bfloat16)
+    out = contract("(i,k),(k,j)->(j,i)", a, b, out_dtype=torch.float32)
+    want = oracle.gemm_kseq(np32(a), np32(b)).T
+    assert oracle.rel_frobenius(np32(out), want) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_baseline_sizes_row_sampled(dev, cfg):
+    """BASELINE C3 (64 x 1024^3) and C4 (4096^3) bf16: full GPU run, oracle on
+    sampled rows of every batch (ladder L1/L2 of SURVEY §8c)."""
+    if cfg == "c3":
+        a, b = rnd((64, 1024, 1024), 1, dev, torch.bfloat16), rnd((64, 1024, 1024), 2, dev, torch.bfloat16)
+        spec = "(b,i,j),(b,j,k)->(b,i,k)"
+    else:
+        a, b = rnd((4096, 4096), 1, dev, torch.bfloat16), rnd((4096, 4096), 2, dev, torch.bfloat16)
+        spec = "(i,k),(k,j)->(i,j)"
+    out = contract(spec, a, b)
+    assert out.dtype == torch.bfloat16
+    rows = np.random.default_rng(9).choice(a.shape[-2], 8, replace=False)
+    A, B, O = np32(a), np32(b), np32(out)
+    if cfg == "c4":
+        A, B, O = A[None], B[None], O[None]
+    for bi in range(0, A.shape[0], max(1, A.shape[0] // 4)):
+        want = oracle.gemm_kseq(np.ascontiguousarray(A[bi][rows]), B[bi])
+        assert oracle.rel_frobenius(O[bi][rows], want) <= BF16_TOL
+    assert np.isfinite(O).all()
+
+
+def test_contract_kernel_selection(dev):
+    a = rnd((256, 256), 1, dev, torch.bfloat16)
+    d = _lib.BgxContractDesc()
+    d.batch, d.M, d.N, d.K = 1, 256, 256, 256
+    d.a = d.b = a.data_ptr()
+    d.out = a.data_ptr()
+    d.a_stride[:] = [0, 256, 1]
+    d.b_stride[:] = [0, 256, 1]
+    d.o_stride[:] = [0, 256, 1]
+    d.in_dtype = d.out_dtype = _lib.BF16
+    assert _lib.load().bgx_contract_kernel(d) == _lib.KERNEL_TC
+    d.a_stride[:] = [0, 255, 1]  # 510-byte rows: not TMA legal
+    assert _lib.load().bgx_contract_kernel(d) == _lib.KERNEL_SIMT16
+    d.mode = _lib.MODE_TC
+    assert _lib.load().bgx_contract_kernel(d) == _lib.ERR_UNSUPPORTED
