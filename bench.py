@@ -1,0 +1,430 @@
+"""bench.py — BASELINE.json's metric ("contraction TFLOP/s and % tensor-core
+peak at 1/2/4/8 B200 vs CPU oracle") on the north-star workload.
+
+Workload (``config.workload``): the sharded 32k-class chain, BASELINE config 5:
+    (i,k),(k,j),(j,l)->(i,l)   I = 32768, K = J = L = 8192, bf16 in, f32
+    accumulate, bf16 out; executed left to right, (A @ B) @ C
+    = 2*I*J*(K+L) = 8,796,093,022,208 flop per step.
+With N GPUs (torchrun) the I rows are split into N contiguous slabs; B and C
+are replicated; there is no data-path collective; value = total flop / max
+over ranks of the device time ("scaling": "strong" — the job is fixed).
+
+One step = one pass of the hot path over the job with inputs resident in HBM
+(the inputs, A 512 MiB and A@B 512 MiB, exceed the 126 MB L2).  ``e2e`` is the
+same metric through the public host-buffer API (``contract_host``): pinned
+host inputs copied in, result copied out, every step.  ``roofline`` is for
+the dominant kernel (tcgen05 GEMM), timed per launch with CUDA events on its
+stream inside the timed region.  ``cpu_baseline`` times the C port of the
+reference's loop nest (oracle/, test infrastructure — only used here as the
+reported baseline) on a bounded sample of output elements on the host cores.
+
+``--impl reference`` prints the reference arm: the oracle port of the
+reference algorithm on all host cores (rank 0 only; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+I_, K_, J_, L_ = 32768, 8192, 8192, 8192
+CHAIN_FLOP = 2 * I_ * J_ * (K_ + L_)
+CHAIN_FLOP_MINORDER = 2 * K_ * J_ * L_ + 2 * I_ * K_ * L_
+SPEC = "(i,k),(k,j),(j,l)->(i,l)"
+WORKLOAD = "chain (i,k),(k,j),(j,l)->(i,l) I=32768 K=J=L=8192 bf16 (BASELINE config 5)"
+METRIC = "contraction TFLOP/s and % tensor-core peak at 1/2/4/8 B200 vs CPU oracle"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return {"bf16": p["bf16_tflops"], "bf16_sustained": p["bf16_tflops_sustained"],
+                "hbm": p["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML, sampled from a thread)
+
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self.period = period_s
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def barrier_sync(world):
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the C port of the reference loop nest (oracle/), bounded sample
+
+def cpu_chain_sample(A_row0, B, C, n_elems: int, threads: int):
+    """Reference semantics for the chain: per output element (0, l) the
+    unfactored sum over (k, j) of (a*b)*c in the reference's order
+    (interp.py:407-420 with the einsum.py:111-117 body)."""
+    import oracle
+    out = np.zeros((1, C.shape[1]), np.float32)
+    t0 = time.perf_counter()
+    oracle.chain3(A_row0, B, C, out, cols=(0, n_elems), threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(A_row0, B, C, budget_s: float = 12.0):
+    threads = len(os.sched_getaffinity(0))
+    probe = 16 * threads   # one 16-wide l block per thread
+    t = cpu_chain_sample(A_row0, B, C, probe, threads)
+    per_elem = t / probe
+    n = max(probe, min(int(budget_s / per_elem), C.shape[1]))
+    n = (n // probe) * probe or probe
+    t = cpu_chain_sample(A_row0, B, C, n, threads)
+    per_elem = t / n
+    total_s = per_elem * I_ * L_
+    return {"value": CHAIN_FLOP / total_s / 1e12, "unit": "TFLOP/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{n} output elements of row 0 (each the reference's unfactored "
+                      f"K*J = {K_ * J_} point loop, oracle.chain3, bit-equal to the "
+                      f"reference order), {t:.1f} s on {threads} threads; "
+                      f"extrapolated job time {total_s:.3e} s",
+            "job_seconds_extrapolated": total_s}
+
+
+# ---------------------------------------------------------------------------
+
+def make_inputs(rows, dev, seed):
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + seed)
+    A = torch.randn((rows, K_), generator=g, device=dev, dtype=torch.float32).bfloat16()
+    g.manual_seed(2)
+    B = torch.randn((K_, J_), generator=g, device=dev, dtype=torch.float32).bfloat16()
+    g.manual_seed(3)
+    C = torch.randn((J_, L_), generator=g, device=dev, dtype=torch.float32).bfloat16()
+    return A, B, C
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.lib()
+    rng = np.random.default_rng(1)
+    A0 = rng.standard_normal((1, K_), dtype=np.float32)
+    B = np.random.default_rng(2).standard_normal((K_, J_), dtype=np.float32)
+    C = np.random.default_rng(3).standard_normal((J_, L_), dtype=np.float32)
+    threads = len(os.sched_getaffinity(0))
+    n = min(16 * threads, L_)  # one 16-wide block of output elements per thread per step
+    for _ in range(args.warmup):
+        cpu_chain_sample(A0, B, C, n, threads)
+    times = [cpu_chain_sample(A0, B, C, n, threads) for _ in range(args.steps)]
+    per_elem = sum(times) / (len(times) * n)
+    total_s = per_elem * I_ * L_
+    value = CHAIN_FLOP / total_s / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": "host cores (OpenMP over outputs)",
+                   "step": f"{n} output elements of the reference loop nest, extrapolated"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} output elements per step x {args.steps} steps"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def time_kernel(fn, iters, flush=None):
+    """Mean device time (ms) of ``fn`` with CUDA events per call, flushing L2
+    between calls when ``flush`` is given."""
+    s = torch.cuda.current_stream()
+    evs = []
+    for _ in range(iters):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+
+def aux_configs(dev, pk):
+    """The other BASELINE configs, N=1: kernel-only numbers (not the headline)."""
+    from paper_2503_04771_b200 import contract
+    from paper_2503_04771_b200 import einsum as E
+    from paper_2503_04771_b200 import interp as I
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = lambda: flush_buf.zero_()  # noqa: E731  (L2 flush, outside the events)
+    res = {}
+    a = torch.randn(4096, 4096, device=dev).bfloat16()
+    b = torch.randn(4096, 4096, device=dev).bfloat16()
+    out = torch.empty(4096, 4096, device=dev, dtype=torch.bfloat16)
+    fn = lambda: contract("(i,k),(k,j)->(i,j)", a, b, out=out)  # noqa: E731
+    for _ in range(3):
+        fn()
+    ms = time_kernel(fn, 20, flush)
+    tf = 2 * 4096 ** 3 / ms / 1e9
+    res["c4_gemm_4096"] = {"ms": ms, "tflops": tf, "frac_of_measured_burst": tf / pk["bf16"]}
+    a = torch.randn(64, 1024, 1024, device=dev).bfloat16()
+    b = torch.randn(64, 1024, 1024, device=dev).bfloat16()
+    out = torch.empty(64, 1024, 1024, device=dev, dtype=torch.bfloat16)
+    fn = lambda: contract("(b,i,j),(b,j,k)->(b,i,k)", a, b, out=out)  # noqa: E731
+    for _ in range(3):
+        fn()
+    ms = time_kernel(fn, 20, flush)
+    tf = 2 * 64 * 1024 ** 3 / ms / 1e9
+    res["c3_batched_64x1024"] = {"ms": ms, "tflops": tf, "frac_of_measured_burst": tf / pk["bf16"]}
+    for name, shape, spec in (("c2a_perm_8192sq", (8192, 8192), "(i,j)->(j,i)"),
+                              ("c2b_perm_256x512x512", (256, 512, 512), "(i,j,k)->(k,j,i)")):
+        x = torch.randn(shape, device=dev)
+        out = torch.empty(tuple(reversed(shape)), device=dev)
+        fn = lambda: contract(spec, x, out=out)  # noqa: E731
+        for _ in range(3):
+            fn()
+        ms = time_kernel(fn, 20, flush)
+        gbs = 2 * x.numel() * 4 / ms / 1e6
+        res[name] = {"ms": ms, "GB/s": gbs, "frac_of_measured_hbm": gbs / pk["hbm"]}
+    # C1: 256^3 f32 through the DSL (reference API), bit-exact SIMT kernel
+    rng = np.random.default_rng(1)
+    a = torch.from_numpy(rng.standard_normal((256, 256), dtype=np.float32)).to(dev)
+    b = torch.from_numpy(rng.standard_normal((256, 256), dtype=np.float32)).to(dev)
+    c = torch.zeros(256, 256, device=dev)
+    mod = E.build_einsum_function(None, E.parse_einsum("(i,j),(j,k)->(i,k)"))
+    vals = [I.TensorValue(E.F32, (256, 256), t) for t in (a, b, c)]
+    fn = lambda: I.run_function(mod, "einsum", vals, step_limit=None)  # noqa: E731
+    for _ in range(3):
+        fn()
+    ms = time_kernel(fn, 20)
+    res["c1_fp32_256_dsl_exact"] = {"ms": ms, "tflops": 2 * 256 ** 3 / ms / 1e9,
+                                    "note": "bit-exact with the reference; launch-bound"}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-aux", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-n", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2503_04771_b200 import _lib, executor, shard
+    from paper_2503_04771_b200.api import contract_host
+    _lib.load()
+    pk = peaks()
+
+    r0, r1 = shard.row_range(I_, world, rank)
+    rows = r1 - r0
+    A, B, C = make_inputs(rows, dev, rank)
+    T = torch.empty((rows, J_), dtype=torch.bfloat16, device=dev)
+    O = torch.empty((rows, L_), dtype=torch.bfloat16, device=dev)
+    sched = {"tile_n": args.tile_n} if args.tile_n else None
+    stream = torch.cuda.current_stream()
+    gemm_events = []
+
+    def gemm(a, b, out, m, n, k, record):
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        executor.contract_raw(a, (0, k, 1), b, (0, n, 1), out, (0, n, 1), batch=1, M=m, N=n,
+                              K=k, mode="tc", schedule=sched)
+        if record:
+            e1.record(stream)
+            gemm_events.append((e0, e1))
+
+    def step(record=False):
+        gemm(A, B, T, rows, J_, K_, record)      # (i,k),(k,j)->(i,j)
+        gemm(T, C, O, rows, L_, J_, record)      # (i,j),(j,l)->(i,l)
+
+    for _ in range(args.warmup):
+        step()
+    barrier_sync(world)
+    executor.reset_launch_log()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(record=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    launches = len(executor.launch_log())
+    barrier_sync(world)
+    ms_local = t0.elapsed_time(t1) / args.steps
+    ms = max_over_ranks(ms_local, world)
+    value = CHAIN_FLOP / (ms * 1e-3) / 1e12
+    gemm_ms = statistics.mean(a.elapsed_time(b) for a, b in gemm_events)
+    gemm_flop = 2 * rows * K_ * J_           # both launches are rows x 8192 x 8192
+    achieved = gemm_flop / (gemm_ms * 1e-3) / 1e12
+
+    # parity on row samples of this shard: f64 factored oracle (ladder L3)
+    import oracle
+    sample = np.random.default_rng(rank).choice(rows, 4, replace=False)
+    a_s = A[torch.as_tensor(sample, device=dev)].float().cpu().numpy()
+    want = oracle.chain_f64(a_s, B.float().cpu().numpy(), C.float().cpu().numpy(), slice(None))
+    got = O[torch.as_tensor(sample, device=dev)].float().cpu().numpy()
+    relF = max_over_ranks(oracle.rel_frobenius(got, want), world)
+
+    # e2e: public host-buffer API, pinned host inputs/outputs, every step
+    e2e = None
+    if not args.no_e2e:
+        hA = torch.empty(A.shape, dtype=A.dtype, pin_memory=True).copy_(A)
+        hB = torch.empty(B.shape, dtype=B.dtype, pin_memory=True).copy_(B)
+        hC = torch.empty(C.shape, dtype=C.dtype, pin_memory=True).copy_(C)
+        hO = torch.empty(O.shape, dtype=O.dtype, pin_memory=True)
+        run = lambda: contract_host(SPEC, hA, hB, hC, out=hO, device=dev)  # noqa: E731
+        e2e_steps = max(3, args.steps // 4)
+        run()
+        barrier_sync(world)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(e2e_steps):
+            run()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(s0.elapsed_time(s1) / e2e_steps, world)
+        e2e = {"value": CHAIN_FLOP / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "ms_per_step": e_ms,
+               "h2d_bytes_per_step": (hA.numel() + hB.numel() + hC.numel()) * 2 * world,
+               "d2h_bytes_per_step": I_ * L_ * 2,
+               "api": "paper_2503_04771_b200.api.contract_host (pinned host buffers)"}
+
+    aux = None
+    cpu = None
+    if rank == 0 and world == 1:
+        if not args.no_aux:
+            aux = aux_configs(dev, pk)
+        if not args.no_cpu:
+            cpu = cpu_baseline(A[:1].float().cpu().numpy(), B.float().cpu().numpy(),
+                               C.float().cpu().numpy())
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("bytes_per_launch")
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (torch.randn on device, bf16-rounded)",
+            "config": {"workload": WORKLOAD, "global_batch": I_, "parallelism": f"M-shard x{world}",
+                       "order": "left-to-right (A@B)@C", "flop_per_step": CHAIN_FLOP,
+                       "flop_min_order": CHAIN_FLOP_MINORDER,
+                       "l2": "inputs exceed L2 (A 512 MiB, A@B 512 MiB per 1-GPU step)"},
+            "fraction_of_peak": value / (pk["bf16"] * world),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"],
+                         "unit": "TFLOP/s", "frac": achieved / pk["bf16"], "traffic": traffic,
+                         "kernel": "tc_gemm_kernel (tcgen05/TMEM/TMA)",
+                         "flop_per_launch": gemm_flop, "launch_ms": gemm_ms,
+                         "peak_source": pk["source"] + " burst bf16",
+                         "frac_of_sustained": achieved / pk["bf16_sustained"]},
+            "parity": {"relF_row_samples_max_over_ranks": relF, "tolerance": 1e-2,
+                       "oracle": "float64 (A@B)@C on the bf16 inputs"},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clk.summary(), "aux": aux,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

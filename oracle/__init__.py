@@ -52,6 +52,10 @@ def lib():
             f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P,
                           _P, _P, _i64, _i64, ctypes.c_int]
             f.restype = ctypes.c_int
+        f = L.oracle_chain3_f32
+        f.argtypes = [_i64, _i64, _i64, _i64, _P, _P, _P, _P, _i64, _i64, _i64, _i64,
+                      ctypes.c_int]
+        f.restype = ctypes.c_int
         f = L.oracle_gemm_kseq_f32
         f.argtypes = [_i64, _i64, _i64, _i64, _P, _i64, _i64, _i64,
                       _P, _i64, _i64, _i64, _P, _P, _i64, _i64, ctypes.c_int]
@@ -131,6 +135,23 @@ def gemm_kseq(a: np.ndarray, b: np.ndarray, c0: np.ndarray | None = None, *,
         b3.ctypes.data, b3.strides[0] // isz, b3.strides[1] // isz, b3.strides[2] // isz,
         c.ctypes.data, c.ctypes.data, lo, hi, threads)
     return c[0] if squeeze else c
+
+
+def chain3(a, b, c, out_init, *, rows=None, cols=None, threads: int = 0):
+    """Reference (unfactored) semantics of (i,k),(k,j),(j,l)->(i,l) in f32,
+    vectorised over l; bit-equal to ``generic`` on the same spec.  Computes
+    rows [r0, r1) x cols [c0, c1) of the result (the rest = out_init)."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    c = np.ascontiguousarray(c, dtype=np.float32)
+    out = np.array(out_init, dtype=np.float32, order="C", copy=True)
+    I, K = a.shape
+    J, L = c.shape
+    r0, r1 = rows if rows is not None else (0, I)
+    c0_, c1_ = cols if cols is not None else (0, L)
+    lib().oracle_chain3_f32(I, K, J, L, a.ctypes.data, b.ctypes.data, c.ctypes.data,
+                            out.ctypes.data, r0, r1, c0_, c1_, threads)
+    return out
 
 
 def chain_f64(a: np.ndarray, b: np.ndarray, c: np.ndarray, rows) -> np.ndarray:

@@ -150,3 +150,48 @@ int oracle_gemm_kseq_f32(int64_t batch, int64_t M, int64_t N, int64_t K,
 }
 
 int oracle_version(void) { return 1; }
+
+/*
+ * The BASELINE config-5 chain (i,k),(k,j),(j,l)->(i,l) with the reference's
+ * UNFACTORED per-point semantics: axes (i, l, k, j) (einsum.py:81), so each
+ * output element accumulates, for k outer and j inner,
+ *     p = fl(a[i,k] * b[k,j]); p = fl(p * c[j,l]); acc = fl(p + acc)
+ * exactly as oracle_generic_f32 / the reference do — but 16 consecutive l are
+ * carried in 16 independent accumulators so the inner loop vectorises over l
+ * (c rows are contiguous).  Each lane's operation sequence is unchanged, so
+ * the bits equal oracle_generic_f32's (tests/test_oracle.py).  Row-major
+ * dense a (I x K), b (K x J), c (J x L), out (I x L) initialised by caller.
+ * Computes rows [i0, i1) x columns [l0, l1).
+ */
+#define CHAIN_LANES 16
+int oracle_chain3_f32(int64_t I, int64_t K, int64_t J, int64_t L,
+                      const float *a, const float *b, const float *c, float *out,
+                      int64_t i0, int64_t i1, int64_t l0, int64_t l1, int threads)
+{
+    (void)I;
+    const int64_t nlb = (l1 - l0 + CHAIN_LANES - 1) / CHAIN_LANES;
+    const int64_t tasks = (i1 - i0) * nlb;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads > 0 ? threads : omp_get_max_threads())
+    for (int64_t t = 0; t < tasks; ++t) {
+        const int64_t i = i0 + t / nlb;
+        const int64_t lb = l0 + (t % nlb) * CHAIN_LANES;
+        const int64_t nl = (l1 - lb) < CHAIN_LANES ? (l1 - lb) : CHAIN_LANES;
+        float acc[CHAIN_LANES];
+        for (int q = 0; q < CHAIN_LANES; ++q) acc[q] = q < nl ? out[i * L + lb + q] : 0.0f;
+        for (int64_t k = 0; k < K; ++k) {
+            const float aik = a[i * K + k];
+            const float *brow = b + k * J;
+            for (int64_t j = 0; j < J; ++j) {
+                const float p = aik * brow[j];
+                const float *crow = c + j * L + lb;
+                if (nl == CHAIN_LANES) {
+                    for (int q = 0; q < CHAIN_LANES; ++q) acc[q] = p * crow[q] + acc[q];
+                } else {
+                    for (int q = 0; q < nl; ++q) acc[q] = p * crow[q] + acc[q];
+                }
+            }
+        }
+        for (int q = 0; q < nl; ++q) out[i * L + lb + q] = acc[q];
+    }
+    return 0;
+}

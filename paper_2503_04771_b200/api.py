@@ -64,3 +64,24 @@ def _contract_widened(spec, operands, c0, out, mode, schedule):
     if not isinstance(plan, GemmPlan):
         raise NotImplementedError("a widened output dtype needs a 2-input contraction")
     return executor.run_gemm(plan, spec, list(operands), c0, out, mode=mode, schedule=schedule)
+
+
+def contract_host(spec, *host_operands: torch.Tensor, out: torch.Tensor | None = None,
+                  device=None, **kw) -> torch.Tensor:
+    """Host-buffer form of ``contract`` (what a numpy/CPU caller of the
+    reference API pays for): copies the operands host→device on the current
+    stream (async when they are pinned), runs the contraction on the device,
+    and copies the result back into ``out`` (a host tensor; pinned for an
+    async copy) or a fresh host tensor.  Synchronises before returning."""
+    device = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    dev_ops = [t.to(device, non_blocking=True) for t in host_operands]
+    c0 = kw.pop("c0", None)
+    if c0 is not None:
+        c0 = c0.to(device, non_blocking=True)
+    res = contract(spec, *dev_ops, c0=c0, **kw)
+    if out is None:
+        out = torch.empty(res.shape, dtype=res.dtype, pin_memory=True)
+    out.copy_(res, non_blocking=True)
+    torch.cuda.current_stream(device).synchronize()
+    return out
