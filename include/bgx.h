@@ -130,7 +130,8 @@ typedef struct {
   int32_t cta_group;  /* 0 = auto; TC: 1 or 2 (CTA pair, M = 256)           */
   int32_t max_ctas;   /* 0 = auto (persistent: one CTA per SM)              */
   int32_t raster;     /* 0 = auto; L2 tile-group width along M              */
-  int32_t reserved[3];
+  int32_t reserved[3]; /* reserved[0] bit 0: skip epilogue stores (timing
+                          probe only — the output is NOT written)            */
 } bgx_schedule;
 
 typedef struct {
@@ -149,6 +150,10 @@ BGX_API int bgx_contract(const bgx_contract_desc *d, void *stream);
 /* Which kernel bgx_contract would launch: 1 = tcgen05, 2 = SIMT exact,
  * 3 = SIMT ffma, 4 = SIMT 16-bit, negative = error. */
 BGX_API int bgx_contract_kernel(const bgx_contract_desc *d);
+/* Tile shape of the tcgen05 path for this descriptor: cta_group (1 = one CTA,
+ * 128-row tiles; 2 = CTA pair, 256-row tiles) and tile_n; both 0 when the
+ * descriptor would not run on tensor cores. */
+BGX_API int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group, int32_t *tile_n);
 
 /* ---- elementwise helpers for multi-GPU K-split -------------------------
  * out[i] = (dtype_out) src[i] for n elements, src f32 (the reduced partials),

@@ -72,6 +72,8 @@ SIGNATURES = {
     "bgx_generic": (ctypes.c_int, [ctypes.POINTER(BgxGenericDesc), _vp]),
     "bgx_contract": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc), _vp]),
     "bgx_contract_kernel": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc)]),
+    "bgx_contract_tile": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
+                                         ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "bgx_cast_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _vp]),
 }
 

@@ -149,6 +149,16 @@ __device__ __forceinline__ void tma_load_3d_cg2(void *dst, const void *tmap, uin
       : "memory");
 }
 
+// One lane of the (fully active) warp returns true; warp-uniform control flow
+// around it lets ptxas keep loop state in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

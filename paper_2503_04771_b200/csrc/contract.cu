@@ -5,6 +5,7 @@ namespace bgx {
 bool tc_legal(const bgx_contract_desc &d, const char **why);
 int contract_tc(const bgx_contract_desc &d, cudaStream_t s);
 int contract_simt(const bgx_contract_desc &d, int kind, cudaStream_t s);
+void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out);
 
 namespace {
 
@@ -84,4 +85,21 @@ extern "C" int bgx_contract(const bgx_contract_desc *d, void *stream) {
   BGX_CHECK_ARG(d->a != nullptr && d->b != nullptr, "bgx_contract: null operand");
   if (kind == KIND_TC) return contract_tc(*d, s);
   return contract_simt(*d, kind, s);
+}
+
+extern "C" int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group, int32_t *tile_n) {
+  BGX_CHECK_ARG(d != nullptr && cta_group != nullptr && tile_n != nullptr,
+                "bgx_contract_tile: null argument");
+  int rc = validate(*d);
+  if (rc) return rc;
+  if (select_kind(*d) != KIND_TC) {
+    *cta_group = 0;
+    *tile_n = 0;
+    return BGX_OK;
+  }
+  int cg = 0, bn = 0;
+  tc_tile_choice(*d, &cg, &bn);
+  *cta_group = cg;
+  *tile_n = bn;
+  return BGX_OK;
 }

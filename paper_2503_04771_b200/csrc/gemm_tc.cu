@@ -4,23 +4,30 @@
 // multiply-accumulate loop (interp.py:407-420 with the einsum.py:111-117 body)
 // for two-input contractions whose axes group into batch / M / N / K.
 //
-// Structure (one CTA per SM, persistent, warp-specialised, 256 threads):
+// Structure (persistent, warp-specialised, 256 threads per CTA):
 //   warp 0      TMA producer (one lane): fills a STAGES-deep ring of A/B
 //               k-blocks, signalling `full[s]` with transaction bytes;
-//   warp 1      MMA issuer (one lane): waits `full[s]`, issues 4 x
-//               tcgen05.mma (K = 16 each) per 64-wide k-block into one of two
-//               TMEM accumulators, frees the slot with tcgen05.commit ->
-//               `empty[s]`, and signals `tmem_full[acc]` after the last k-block;
-//   warp 2      TMEM allocator (2 x BN columns);
+//   warp 1      MMA issuer (one lane, leader CTA only): waits `full[s]`,
+//               issues 4 x tcgen05.mma (K = 16 each) per 64-wide k-block into
+//               one of two TMEM accumulators, frees the slot with
+//               tcgen05.commit -> `empty[s]`, and signals `tmem_full[acc]`
+//               after the last k-block;
+//   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulator);
 //   warps 4..7  epilogue: wait `tmem_full[acc]`, tcgen05.ld 32 lanes x 32
 //               columns per step, add c0 (beta = 1 semantics of
 //               interp.py:399), convert, store; then arrive `tmem_empty[acc]`
 //               so the MMA warp can reuse the accumulator — the epilogue of
 //               tile i overlaps the main loop of tile i+1.
-// Tiles: 128 (M) x BN (N) x 64 (K); batch folded into the tile index; tile
-// order is rasterised in groups of `raster` M-tiles for L2 reuse.
-// Operand layouts: A K-major or M-major, B K-major or N-major — the major-ness
-// goes into the instruction descriptor, no transposing copy is made.
+// CG = 1: one CTA per SM computes 128 x BN tiles (tcgen05.mma cta_group::1).
+// CG = 2: a cluster of 2 CTAs on one TPC computes 256 x BN tiles with
+//   tcgen05.mma.cta_group::2 (M = 256): each CTA stages its 128 rows of A and
+//   its BN/2 columns of B (TMA .cta_group::2 signals the leader's barrier), the
+//   leader issues the MMAs, each CTA's TMEM holds its 128 accumulator rows.
+//   Per SM this halves the shared-memory and L2->SM bytes of B per flop.
+// Tiles: BK = 64; batch folded into the tile index; tile order rasterised in
+// groups of `raster` M-tiles for L2 reuse.  Operand layouts: A K- or M-major,
+// B K- or N-major — the major-ness goes into the instruction descriptor, no
+// transposing copy is made.
 #include "common.cuh"
 
 #include <cudaTypedefs.h>
@@ -30,10 +37,11 @@ namespace bgx {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BK = 64;                 // 64 x 16-bit = 128 B = one swizzle row
+constexpr int BM = 128;                     // rows of A per CTA
+constexpr int BK = 64;                      // 64 x 16-bit = 128 B = one swizzle row
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int NUM_THREADS = 256;
+constexpr int SMEM_BUDGET = 227 * 1024;
 
 struct TcParams {
   int64_t batch, M, N, K;
@@ -41,16 +49,21 @@ struct TcParams {
   int64_t num_tiles;
   uint32_t idesc;
   int32_t a_mn, b_mn;            // 1 = MN-major operand
+  int32_t stages;                // ring depth actually used (<= Cfg::STAGES)
+  int32_t debug;                 // bit 0: skip the epilogue stores (timing probe)
   const void *c0; int64_t sc[3];
   void *out; int64_t so[3];
 };
 
-template <int BN> struct Cfg {
-  static constexpr int B_STAGE_BYTES = BN * BK * 2;
+template <int BN, int CG> struct Cfg {
+  static constexpr int BN_CTA = BN / CG;                 // B columns staged per CTA
+  static constexpr int B_STAGE_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TILE_M = BM * CG;
 };
 
 __device__ __forceinline__ void tile_coords(const TcParams &p, int64_t t, int64_t &b, int64_t &tm,
@@ -102,25 +115,38 @@ template <typename H> struct Store16 {
 template <> struct Store<__nv_bfloat16> : Store16<__nv_bfloat16> {};
 template <> struct Store<__half> : Store16<__half> {};
 
-template <int BN, typename OutT>
+template <int CG>
+__device__ __forceinline__ void tma_load(void *dst, const void *tmap, uint64_t *bar, int32_t c0,
+                                         int32_t c1, int32_t c2) {
+  if constexpr (CG == 1) tma_load_3d(dst, tmap, bar, c0, c1, c2);
+  else tma_load_3d_cg2(dst, tmap, bar, c0, c1, c2);
+}
+
+template <int BN, int CG, typename OutT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                const __grid_constant__ CUtensorMap tmap_b, const TcParams p) {
-  using C = Cfg<BN>;
-  constexpr int STAGES = C::STAGES;
+  using C = Cfg<BN, CG>;
+  constexpr int MAX_STAGES = C::STAGES;
+  const int STAGES = p.stages;
+  constexpr int BN_CTA = C::BN_CTA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *smem_a = smem;
-  uint8_t *smem_b = smem + STAGES * A_STAGE_BYTES;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t *smem_b = smem + MAX_STAGES * A_STAGE_BYTES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + MAX_STAGES * C::STAGE_BYTES);
   uint64_t *full = bars;
-  uint64_t *empty = bars + STAGES;
-  uint64_t *tmem_full = bars + 2 * STAGES;
-  uint64_t *tmem_empty = bars + 2 * STAGES + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+  uint64_t *empty = bars + MAX_STAGES;
+  uint64_t *tmem_full = bars + 2 * MAX_STAGES;
+  uint64_t *tmem_empty = bars + 2 * MAX_STAGES + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * MAX_STAGES + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = CG == 1 ? 0 : cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t cluster_id = blockIdx.x / CG;
+  const int64_t num_clusters = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
@@ -131,61 +157,68 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 128);
+      mbar_init(&tmem_empty[a], 4 * CG);  // one arrive per epilogue warp per CTA
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    tmem_alloc<1>(tmem_slot, C::TMEM_COLS);
-    tmem_relinquish<1>();
+    tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish<CG>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer =====
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int64_t b, tm, tn;
-        tile_coords(p, t, b, tm, tn);
-        const int32_t m0 = (int32_t)(tm * BM), n0 = (int32_t)(tn * BN), bb = (int32_t)b;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+    // ===== TMA producer (every CTA loads its own A rows / B columns) =====
+    // Warp-uniform loop; one elected lane issues the barrier ops and copies.
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+      int64_t b, tm, tn;
+      tile_coords(p, t, b, tm, tn);
+      const int32_t m0 = (int32_t)(tm * C::TILE_M + rank * BM);
+      const int32_t n0 = (int32_t)(tn * BN + rank * BN_CTA);
+      const int32_t bb = (int32_t)b;
+      for (int kb = 0; kb < p.k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
           const int32_t k0 = kb * BK;
           uint8_t *sa = smem_a + stage * A_STAGE_BYTES;
           uint8_t *sb = smem_b + stage * C::B_STAGE_BYTES;
           if (p.a_mn) {
-            tma_load_3d(sa, &tmap_a, &full[stage], m0, k0, bb);
-            tma_load_3d(sa + 8192, &tmap_a, &full[stage], m0 + 64, k0, bb);
+            tma_load<CG>(sa, &tmap_a, &full[stage], m0, k0, bb);
+            tma_load<CG>(sa + 8192, &tmap_a, &full[stage], m0 + 64, k0, bb);
           } else {
-            tma_load_3d(sa, &tmap_a, &full[stage], k0, m0, bb);
+            tma_load<CG>(sa, &tmap_a, &full[stage], k0, m0, bb);
           }
           if (p.b_mn) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_3d(sb + j * 8192, &tmap_b, &full[stage], n0 + 64 * j, k0, bb);
+            for (int j = 0; j < BN_CTA / 64; ++j)
+              tma_load<CG>(sb + j * 8192, &tmap_b, &full[stage], n0 + 64 * j, k0, bb);
           } else {
-            tma_load_3d(sb, &tmap_b, &full[stage], k0, n0, bb);
+            tma_load<CG>(sb, &tmap_b, &full[stage], k0, n0, bb);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
+    if (leader) {
+      // ===== MMA issuer: warp-uniform loop, one elected lane issues =====
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      // per-k16 descriptor advance and fixed LBO/SBO per operand layout
-      const uint32_t a_step = p.a_mn ? 2048u : 32u, b_step = p.b_mn ? 2048u : 32u;
-      const uint32_t a_lbo = p.a_mn ? 8192u : 16u, b_lbo = p.b_mn ? 8192u : 16u;
-      for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+      // Descriptor = {lo: start>>4 | LBO>>4 << 16, hi: SBO>>4 | version | SW128}:
+      // only the start-address field moves along K, so precompute the rest.
+      const uint32_t a_step = (p.a_mn ? 2048u : 32u) >> 4, b_step = (p.b_mn ? 2048u : 32u) >> 4;
+      const uint64_t a_fixed = make_sdesc_sw128(0, p.a_mn ? 8192u : 16u, 1024);
+      const uint64_t b_fixed = make_sdesc_sw128(0, p.b_mn ? 8192u : 16u, 1024);
+      const uint32_t sa0 = smem_u32(smem_a) >> 4, sb0 = smem_u32(smem_b) >> 4;
+      for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -194,32 +227,37 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         for (int kb = 0; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem_a + stage * A_STAGE_BYTES);
-          const uint32_t sb = smem_u32(smem_b + stage * C::B_STAGE_BYTES);
+          if (elect_one()) {
+            const uint64_t ad0 = a_fixed | (uint64_t)(sa0 + stage * (A_STAGE_BYTES >> 4));
+            const uint64_t bd0 = b_fixed | (uint64_t)(sb0 + stage * (C::B_STAGE_BYTES >> 4));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = make_sdesc_sw128(sa + k * a_step, a_lbo, 1024);
-            const uint64_t bd = make_sdesc_sw128(sb + k * b_step, b_lbo, 1024);
-            umma_f16<1>(d_tmem, ad, bd, p.idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / 16; ++k)
+              umma_f16<CG>(d_tmem, ad0 + k * a_step, bd0 + k * b_step, p.idesc, (kb | k) != 0);
+            if constexpr (CG == 1) umma_commit(&empty[stage]);
+            else umma_commit_mc(&empty[stage], 0x3);
           }
-          umma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tmem_full[acc]);
+        if (elect_one()) {
+          if constexpr (CG == 1) umma_commit(&tmem_full[acc]);
+          else umma_commit_mc(&tmem_full[acc], 0x3);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
-    // ===== epilogue =====
+    // ===== epilogue (every CTA drains its own 128 TMEM lanes) =====
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
     int it = 0;
-    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++it) {
+    for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = tm * BM + ew * 32 + lane;
+      const int64_t m = tm * C::TILE_M + rank * BM + ew * 32 + lane;
       const bool row_ok = m < p.M;
       OutT *orow = static_cast<OutT *>(p.out) + b * p.so[0] + m * p.so[1];
       const OutT *crow = p.c0 ? static_cast<const OutT *>(p.c0) + b * p.sc[0] + m * p.sc[1] : nullptr;
@@ -229,7 +267,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int64_t n = tn * BN + c * 32;
-        if (row_ok && n < p.N) {
+        if (row_ok && n < p.N && !(p.debug & 1)) {
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
@@ -242,14 +280,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         }
       }
       tc_fence_before();
-      mbar_arrive(&tmem_empty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&tmem_empty[acc]);
+        else mbar_arrive_cluster(&tmem_empty[acc], 0);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem_base, C::TMEM_COLS);
+    tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
   }
 }
 
@@ -293,9 +335,31 @@ int make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int64_t
   return BGX_OK;
 }
 
-template <int BN, typename OutT>
+// Max co-resident clusters for a kernel config, cached per (device, kernel).
+template <typename K>
+int max_clusters(K kern, int smem, int cg) {
+  int n = 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * 148);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cg;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+template <int BN, int CG, typename OutT>
 int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   TcParams p = p0;
   const CUtensorMapDataType dt =
       d.in_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -309,33 +373,77 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   if (p.b_mn)
     rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], 64, 64);
   else
-    rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], 64, BN);
+    rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], 64, C::BN_CTA);
   if (rc) return rc;
-  p.idesc = make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, BM, BN);
+  p.idesc = make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, BN);
+  p.stages = (d.sched.stages >= 2 && d.sched.stages <= C::STAGES) ? d.sched.stages : C::STAGES;
+  p.tiles_m = (int32_t)((d.M + C::TILE_M - 1) / C::TILE_M);
   p.tiles_n = (int32_t)((d.N + BN - 1) / BN);
   p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * d.batch;
-  auto kern = tc_gemm_kernel<BN, OutT>;
+  auto kern = tc_gemm_kernel<BN, CG, OutT>;
   static thread_local int configured[64] = {0};
+  static thread_local int clusters[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 63]) {
     BGX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM_BYTES));
     configured[dev & 63] = 1;
+    clusters[dev & 63] = CG == 1 ? sm_count_current() : max_clusters(kern, C::SMEM_BYTES, CG);
+    if (clusters[dev & 63] <= 0) clusters[dev & 63] = sm_count_current() / CG;
   }
-  int sms = sm_count_current();
-  int64_t grid = p.num_tiles < sms ? p.num_tiles : sms;
-  if (d.sched.max_ctas > 0 && grid > d.sched.max_ctas) grid = d.sched.max_ctas;
-  kern<<<(unsigned)grid, NUM_THREADS, C::SMEM_BYTES, s>>>(ma, mb, p);
+  int64_t nclusters = clusters[dev & 63];
+  if (p.num_tiles < nclusters) nclusters = p.num_tiles;
+  if (d.sched.max_ctas > 0 && nclusters * CG > d.sched.max_ctas) nclusters = d.sched.max_ctas / CG;
+  if (nclusters < 1) nclusters = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(nclusters * CG));
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BGX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, p));
   return check_launch("tc_gemm_kernel");
 }
 
-template <typename OutT>
+template <int CG, typename OutT>
 int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStream_t s) {
   switch (bn) {
-    case 64: return launch_tc<64, OutT>(d, p, s);
-    case 128: return launch_tc<128, OutT>(d, p, s);
-    default: return launch_tc<256, OutT>(d, p, s);
+    case 64: return CG == 1 ? launch_tc<64, 1, OutT>(d, p, s) : launch_tc<128, CG, OutT>(d, p, s);
+    case 128: return launch_tc<128, CG, OutT>(d, p, s);
+    default: return launch_tc<256, CG, OutT>(d, p, s);
+  }
+}
+
+// Tile choice: minimise waves x per-CTA tile area / efficiency over the
+// candidate (CG, BN) shapes.  A CTA's time per tile is proportional to its
+// tile area at the full per-SM MMA rate, scaled by the shape's measured
+// efficiency (round-1 sweeps on B200, scripts/sweep_gemm.py: narrower tiles
+// pay relatively more epilogue / A-operand traffic per flop, single CTAs more
+// L2->SM bytes of B).  A later candidate must be >3 % cheaper to win.
+void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
+  struct Cand { int cg, bn; double eff; };
+  const Cand cands[] = {{2, 256, 1.00}, {2, 128, 0.85}, {1, 256, 0.88}, {1, 128, 0.80},
+                        {1, 64, 0.60}};
+  double best = -1.0;
+  for (const Cand &c : cands) {
+    if (c.bn > 64 && d.N <= c.bn / 2) continue;  // tiles would be mostly empty
+    const int64_t tm = (d.M + 128 * c.cg - 1) / (128 * c.cg);
+    const int64_t tn = (d.N + c.bn - 1) / c.bn;
+    const int64_t slots = sms / c.cg;
+    const int64_t waves = (tm * tn * d.batch + slots - 1) / slots;
+    const double cost = (double)waves * (double)(128 * c.bn) / c.eff;
+    if (best < 0 || cost < best * 0.97) {
+      best = cost;
+      cg = c.cg;
+      bn = c.bn;
+    }
   }
 }
 
@@ -365,6 +473,8 @@ bool tc_legal(const bgx_contract_desc &d, const char **why) {
   return true;
 }
 
+void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out);
+
 int contract_tc(const bgx_contract_desc &d, cudaStream_t s) {
   const char *why = nullptr;
   if (!tc_legal(d, &why)) {
@@ -375,16 +485,30 @@ int contract_tc(const bgx_contract_desc &d, cudaStream_t s) {
   p.batch = d.batch; p.M = d.M; p.N = d.N; p.K = d.K;
   p.a_mn = d.a_stride[2] != 1 ? 1 : 0;
   p.b_mn = d.b_stride[2] == 1 ? 1 : 0;
-  p.tiles_m = (int32_t)((d.M + BM - 1) / BM);
   p.k_blocks = (int32_t)((d.K + BK - 1) / BK);
-  p.raster = d.sched.raster > 0 ? d.sched.raster : 16;
   p.c0 = d.c0; p.out = d.out;
   for (int i = 0; i < 3; ++i) { p.sc[i] = d.c_stride[i]; p.so[i] = d.o_stride[i]; }
-  int bn = d.sched.tile_n;
-  if (bn != 64 && bn != 128 && bn != 256) bn = d.N <= 64 ? 64 : (d.N <= 128 ? 128 : 256);
-  if (d.out_dtype == BGX_F32) return dispatch_bn<float>(d, bn, p, s);
-  if (d.out_dtype == BGX_BF16) return dispatch_bn<__nv_bfloat16>(d, bn, p, s);
-  return dispatch_bn<__half>(d, bn, p, s);
+  int cg = 0, bn = 0;
+  tc_tile_choice(d, &cg, &bn);
+  p.raster = d.sched.raster > 0 ? d.sched.raster : (cg == 2 ? 8 : 16);
+  p.debug = d.sched.reserved[0];
+  if (d.out_dtype == BGX_F32)
+    return cg == 2 ? dispatch_bn<2, float>(d, bn, p, s) : dispatch_bn<1, float>(d, bn, p, s);
+  if (d.out_dtype == BGX_BF16)
+    return cg == 2 ? dispatch_bn<2, __nv_bfloat16>(d, bn, p, s)
+                   : dispatch_bn<1, __nv_bfloat16>(d, bn, p, s);
+  return cg == 2 ? dispatch_bn<2, __half>(d, bn, p, s) : dispatch_bn<1, __half>(d, bn, p, s);
+}
+
+// Tile shape the TC path would use (bgx_contract_tile).
+void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out) {
+  int cg = 0, bn = 0;
+  choose_tile(d, sm_count_current(), cg, bn);
+  if (d.sched.cta_group == 1 || d.sched.cta_group == 2) cg = d.sched.cta_group;
+  if (d.sched.tile_n == 64 || d.sched.tile_n == 128 || d.sched.tile_n == 256) bn = d.sched.tile_n;
+  if (cg == 2 && bn == 64) bn = 128;
+  *cg_out = cg;
+  *bn_out = bn;
 }
 
 }  // namespace bgx

@@ -94,13 +94,15 @@ LAYOUTS = {
 @pytest.mark.parametrize("layout", list(LAYOUTS))
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 640), (200, 136, 72), (1000, 520, 1000)])
-def test_tcgen05_layouts(dev, layout, dtype, M, N, K):
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_tcgen05_layouts(dev, layout, dtype, M, N, K, cta_group):
     spec = E.parse_einsum(LAYOUTS[layout])
     shp = {"i": M, "j": N, "k": K}
     a = rnd(tuple(shp[x] for x in spec.inputs[0]), 11, dev, dtype)
     b = rnd(tuple(shp[x] for x in spec.inputs[1]), 12, dev, dtype)
     executor.reset_launch_log()
-    out = contract(spec, a, b, out_dtype=torch.float32, mode="tc")
+    out = contract(spec, a, b, out_dtype=torch.float32, mode="tc",
+                   schedule={"cta_group": cta_group})
     assert executor.launch_log() == ["tcgen05"]
     A = np32(a) if spec.inputs[0] == ("i", "k") else np32(a).T
     B = np32(b) if spec.inputs[1] == ("k", "j") else np32(b).T
@@ -112,10 +114,12 @@ def test_tcgen05_layouts(dev, layout, dtype, M, N, K):
 
 
 @pytest.mark.parametrize("tile_n", [64, 128, 256])
-def test_tcgen05_tile_sizes_and_bf16_out(dev, tile_n):
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_tcgen05_tile_sizes_and_bf16_out(dev, tile_n, cta_group):
     a, b = rnd((384, 320), 21, dev, torch.bfloat16), rnd((320, 448), 22, dev, torch.bfloat16)
     c0 = rnd((384, 448), 23, dev, torch.bfloat16)
-    out = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="tc", schedule={"tile_n": tile_n})
+    out = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="tc",
+                   schedule={"tile_n": tile_n, "cta_group": cta_group})
     assert out.dtype == torch.bfloat16
     want = oracle.gemm_kseq(np32(a), np32(b), np32(c0))
     assert oracle.rel_frobenius(np32(out), want) <= BF16_TOL
@@ -177,3 +181,20 @@ def test_contract_kernel_selection(dev):
     assert _lib.load().bgx_contract_kernel(d) == _lib.KERNEL_SIMT16
     d.mode = _lib.MODE_TC
     assert _lib.load().bgx_contract_kernel(d) == _lib.ERR_UNSUPPORTED
+
+
+def test_tile_choice_abi(dev):
+    """bgx_contract_tile reports the wave-quantisation-driven tile choice."""
+    import ctypes
+    a = rnd((8, 8), 1, dev, torch.bfloat16)
+    d = _lib.BgxContractDesc()
+    d.a = d.b = d.out = a.data_ptr()
+    d.in_dtype = d.out_dtype = _lib.BF16
+    cg, bn = ctypes.c_int32(), ctypes.c_int32()
+    for (M, N, K) in [(4096, 4096, 4096), (32768, 8192, 8192), (256, 64, 4096)]:
+        d.batch, d.M, d.N, d.K = 1, M, N, K
+        d.a_stride[:] = [0, K, 1]
+        d.b_stride[:] = [0, N, 1]
+        d.o_stride[:] = [0, N, 1]
+        assert _lib.load().bgx_contract_tile(d, cg, bn) == 0
+        assert cg.value in (1, 2) and bn.value in (64, 128, 256)
