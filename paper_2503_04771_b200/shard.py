@@ -58,22 +58,19 @@ def _cast(src: torch.Tensor, out: torch.Tensor, c0: torch.Tensor | None):
     return out
 
 
-def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
-                    c0: torch.Tensor | None = None, out_dtype=None, group=None,
-                    scatter: bool = False) -> torch.Tensor:
-    """K-split 2-operand contraction.  ``a_slab``/``b_slab`` hold this rank's
-    K range (the reduction index of ``spec``).  Returns the full reduced
-    output on every rank (``scatter=False``) or this rank's row slab of it
-    (``scatter=True``, reduce-scatter)."""
-    if not isinstance(spec, EinsumSpec):
-        spec = parse_einsum(spec)
-    partial = contract(spec, a_slab, b_slab, out_dtype=torch.float32)
+def ksplit_reduce(partial: torch.Tensor, *, c0: torch.Tensor | None = None, out_dtype=None,
+                  group=None, scatter: bool = False, cast=None) -> torch.Tensor:
+    """Reduce this rank's f32 partial sums of a K-split contraction over the
+    process group — ``reduce_scatter_tensor`` (each rank keeps its row slab)
+    when ``scatter`` and the rows divide evenly, else ``all_reduce`` — then
+    add ``c0`` and cast to ``out_dtype`` with ``bgx_cast_f32``.  ``cast`` is
+    injectable only so the collective logic can be tested on CPU with gloo."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    dt = out_dtype or a_slab.dtype
+    dt = out_dtype or partial.dtype
     if world > 1 and scatter and partial.shape[0] % world == 0:
         rows = partial.shape[0] // world
         red = torch.empty((rows, *partial.shape[1:]), dtype=torch.float32, device=partial.device)
-        dist.reduce_scatter_tensor(red, partial, op=dist.ReduceOp.SUM, group=group)
+        dist.reduce_scatter_tensor(red, partial.contiguous(), op=dist.ReduceOp.SUM, group=group)
         r = dist.get_rank(group)
         c0_local = c0[r * rows:(r + 1) * rows] if c0 is not None else None
     else:
@@ -83,4 +80,20 @@ def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
     if dt == torch.float32 and c0_local is None:
         return red
     out = torch.empty(red.shape, dtype=dt, device=red.device)
-    return _cast(red.contiguous(), out, c0_local.contiguous() if c0_local is not None else None)
+    fn = cast or _cast
+    return fn(red.contiguous(), out, c0_local.contiguous() if c0_local is not None else None)
+
+
+def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
+                    c0: torch.Tensor | None = None, out_dtype=None, group=None,
+                    scatter: bool = False) -> torch.Tensor:
+    """K-split 2-operand contraction.  ``a_slab``/``b_slab`` hold this rank's
+    K range (``k_range``) of the reduction index of ``spec``.  The local
+    partial is a tcgen05 (or SIMT) contraction with f32 output; the partials
+    are then combined by ``ksplit_reduce`` (one NCCL collective).  Returns the
+    full output on every rank, or this rank's row slab with ``scatter``."""
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    partial = contract(spec, a_slab, b_slab, out_dtype=torch.float32)
+    return ksplit_reduce(partial, c0=c0, out_dtype=out_dtype or a_slab.dtype, group=group,
+                         scatter=scatter)
