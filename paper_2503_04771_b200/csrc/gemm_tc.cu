@@ -32,6 +32,7 @@
 
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <string.h>
 
 namespace bgx {
 
@@ -50,19 +51,24 @@ struct TcParams {
   uint32_t idesc;
   int32_t a_mn, b_mn;            // 1 = MN-major operand
   int32_t stages;                // ring depth actually used (<= Cfg::STAGES)
+  int32_t tma_store;             // 1: epilogue stores through TMA (out map legal)
   int32_t debug;                 // bit 0: skip the epilogue stores (timing probe)
   const void *c0; int64_t sc[3];
   void *out; int64_t so[3];
 };
 
-template <int BN, int CG> struct Cfg {
+template <int BN, int CG, int OUT_BYTES> struct Cfg {
   static constexpr int BN_CTA = BN / CG;                 // B columns staged per CTA
   static constexpr int B_STAGE_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048) / STAGE_BYTES;
+  // epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols) of the output
+  static constexpr int EPI_BUF_BYTES = 32 * 32 * OUT_BYTES;
+  static constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
+  static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TILE_M = BM * CG;
 };
 
@@ -78,6 +84,34 @@ __device__ __forceinline__ void tile_coords(const TcParams &p, int64_t t, int64_
   const int64_t gm = (p.tiles_m - first_m) < G ? (p.tiles_m - first_m) : G;
   tm = first_m + in_group % gm;
   tn = in_group / gm;
+}
+
+// Write one thread's row of 32 output values into the warp's swizzled staging
+// buffer (32 rows x 32 cols) in the layout the output tensor map's swizzle
+// expects: SW64 for 16-bit outputs (64-byte rows), SW128 for f32 (128-byte
+// rows): 16-byte chunk j of row r lands at chunk j ^ f(r).
+template <typename OutT>
+__device__ __forceinline__ void stage_row32(uint8_t *buf, int r, const float *v) {
+  if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      *reinterpret_cast<float4 *>(buf + r * 128 + ((j ^ (r & 7)) << 4)) = q;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 pk;
+      uint32_t *w = reinterpret_cast<uint32_t *>(&pk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        OutT lo = Conv<OutT>::from_f(v[8 * j + 2 * q]), hi = Conv<OutT>::from_f(v[8 * j + 2 * q + 1]);
+        w[q] = (uint32_t)(*reinterpret_cast<uint16_t *>(&lo)) |
+               ((uint32_t)(*reinterpret_cast<uint16_t *>(&hi)) << 16);
+      }
+      *reinterpret_cast<uint4 *>(buf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) = pk;
+    }
+  }
 }
 
 template <typename OutT> struct Store;
@@ -125,8 +159,9 @@ __device__ __forceinline__ void tma_load(void *dst, const void *tmap, uint64_t *
 template <int BN, int CG, typename OutT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
-               const __grid_constant__ CUtensorMap tmap_b, const TcParams p) {
-  using C = Cfg<BN, CG>;
+               const __grid_constant__ CUtensorMap tmap_b,
+               const __grid_constant__ CUtensorMap tmap_o, const TcParams p) {
+  using C = Cfg<BN, CG, (int)sizeof(OutT)>;
   constexpr int MAX_STAGES = C::STAGES;
   const int STAGES = p.stages;
   constexpr int BN_CTA = C::BN_CTA;
@@ -134,7 +169,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   uint8_t *smem = reinterpret_cast<uint8_t *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *smem_a = smem;
   uint8_t *smem_b = smem + MAX_STAGES * A_STAGE_BYTES;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + MAX_STAGES * C::STAGE_BYTES);
+  uint8_t *smem_epi = smem + MAX_STAGES * C::STAGE_BYTES;   // 1024-B aligned
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem_epi + C::EPI_BYTES);
   uint64_t *full = bars;
   uint64_t *empty = bars + MAX_STAGES;
   uint64_t *tmem_full = bars + 2 * MAX_STAGES;
@@ -151,6 +187,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_b);
+    if (p.tma_store) prefetch_tmap(&tmap_o);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -249,7 +286,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   } else if (warp >= 4) {
     // ===== epilogue (every CTA drains its own 128 TMEM lanes) =====
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
-    int it = 0;
+    uint8_t *ebuf = smem_epi + ew * 2 * C::EPI_BUF_BYTES;
+    int it = 0, chunk = 0;
     for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
@@ -257,7 +295,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int64_t m = tm * C::TILE_M + rank * BM + ew * 32 + lane;
+      const int64_t m_warp = tm * C::TILE_M + rank * BM + ew * 32;
+      const int64_t m = m_warp + lane;
       const bool row_ok = m < p.M;
       OutT *orow = static_cast<OutT *>(p.out) + b * p.so[0] + m * p.so[1];
       const OutT *crow = p.c0 ? static_cast<const OutT *>(p.c0) + b * p.sc[0] + m * p.sc[1] : nullptr;
@@ -267,15 +306,28 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         const int64_t n = tn * BN + c * 32;
-        if (row_ok && n < p.N && !(p.debug & 1)) {
-          float v[32];
+        if (n >= p.N || (p.debug & 1)) continue;  // warp-uniform
+        float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          const int64_t valid = p.N - n;
-          if (crow) {
-            for (int j = 0; j < 32; ++j)
-              if (j < valid) v[j] = __fadd_rn(v[j], Conv<OutT>::to_f(crow[n + j]));
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        const int64_t valid = p.N - n;
+        if (crow && row_ok) {
+          for (int j = 0; j < 32; ++j)
+            if (j < valid) v[j] = __fadd_rn(v[j], Conv<OutT>::to_f(crow[n + j]));
+        }
+        if (p.tma_store) {
+          uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
+          ++chunk;
+          if (lane == 0) bulk_wait_read<1>();   // the buffer used two chunks ago is free
+          __syncwarp();
+          stage_row32<OutT>(buf, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmap_o, buf, (int32_t)n, (int32_t)m_warp, (int32_t)b);
+            bulk_commit();
           }
+        } else if (row_ok) {
           Store<OutT>::row32(orow + n, v, valid >= 32, valid);
         }
       }
@@ -286,6 +338,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         else mbar_arrive_cluster(&tmem_empty[acc], 0);
       }
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   }
   tc_fence_before();
   if constexpr (CG == 1) __syncthreads(); else cluster_sync();
@@ -311,20 +365,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 3-D map over a 16-bit tensor: dims (inner, outer, batch) with element
-// strides (1, s_outer, s_batch); box (box_inner, box_outer, 1), 128B swizzle.
+// 3-D map: dims (inner, outer, batch) with element strides (1, s_outer,
+// s_batch); box (box_inner, box_outer, 1); 128B swizzle unless given.
 int make_map(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int64_t inner,
              int64_t outer, int64_t batch, int64_t s_outer, int64_t s_batch, uint32_t box_inner,
-             uint32_t box_outer) {
+             uint32_t box_outer, int esize = 2,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return BGX_ERR_CUDA; }
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)batch};
   if (batch <= 1) s_batch = s_outer * outer;  // any legal value; never stepped
-  cuuint64_t strides[2] = {(cuuint64_t)(s_outer * 2), (cuuint64_t)(s_batch * 2)};
+  cuuint64_t strides[2] = {(cuuint64_t)(s_outer * esize), (cuuint64_t)(s_batch * esize)};
   cuuint32_t box[3] = {box_inner, box_outer, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, dt, 3, const_cast<void *>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): dims %lld x %lld x %lld strides %lld/%lld",
@@ -359,7 +414,7 @@ int max_clusters(K kern, int smem, int cg) {
 
 template <int BN, int CG, typename OutT>
 int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, (int)sizeof(OutT)>;
   TcParams p = p0;
   const CUtensorMapDataType dt =
       d.in_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
@@ -375,6 +430,21 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   else
     rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], 64, C::BN_CTA);
   if (rc) return rc;
+  // output map for the TMA-store epilogue (falls back to direct stores when
+  // the output's row/batch strides are not 16-byte multiples)
+  CUtensorMap mo;
+  memset(&mo, 0, sizeof(mo));
+  const int oes = (int)sizeof(OutT);
+  p.tma_store = ((uintptr_t)d.out % 16 == 0) && (d.o_stride[1] * oes) % 16 == 0 &&
+                (d.batch <= 1 || (d.o_stride[0] * oes) % 16 == 0) && !(p.debug & 2);
+  if (p.tma_store) {
+    const CUtensorMapDataType odt = oes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                   : (d.out_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    rc = make_map(&mo, d.out, odt, d.N, d.M, d.batch, d.o_stride[1], d.o_stride[0], 32, 32, oes,
+                  oes == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
   p.idesc = make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, BN);
   p.stages = (d.sched.stages >= 2 && d.sched.stages <= C::STAGES) ? d.sched.stages : C::STAGES;
   p.tiles_m = (int32_t)((d.M + C::TILE_M - 1) / C::TILE_M);
@@ -408,7 +478,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BGX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, p));
+  BGX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, p));
   return check_launch("tc_gemm_kernel");
 }
 

@@ -89,6 +89,52 @@ transpose_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t nx, int6
   }
 }
 
+// ---- vectorised transpose (fast path) ------------------------------------
+// Both unit-stride dims (input's X, output's Y) are contiguous and every other
+// stride is a multiple of the 16-byte vector: threads move 16-byte vectors on
+// both sides, the tile is staged in padded shared memory, the grid is 3-D
+// (x tile, y tile, batch) so no per-element division is needed.  Extents of X
+// and Y are multiples of VEC, so vectors never straddle an edge.
+template <typename T>
+__global__ void __launch_bounds__(256)
+transpose_vec_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t nx, int64_t ny,
+                     int64_t in_sy, int64_t out_sx, BatchDims bd) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TPR = TILE / VEC;          // threads per tile row (vectors per row)
+  constexpr int RPP = 256 / TPR;           // rows per pass
+  __shared__ T tile[TILE][TILE + 1];
+  int64_t in_off, out_off;
+  decode_batch(bd, blockIdx.z, in_off, out_off);
+  const int64_t x0 = (int64_t)blockIdx.x * TILE, y0 = (int64_t)blockIdx.y * TILE;
+  const int tv = threadIdx.x % TPR, tr = threadIdx.x / TPR;
+  // read: rows of the input (fixed y), 16-byte vectors along x
+  const T *src = in + in_off + x0 + (int64_t)tv * VEC;
+#pragma unroll
+  for (int r = tr; r < TILE; r += RPP) {
+    const int64_t y = y0 + r;
+    if (y < ny && x0 + tv * VEC < nx) {
+      uint4 v = __ldcs(reinterpret_cast<const uint4 *>(src + y * in_sy));
+      const T *e = reinterpret_cast<const T *>(&v);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) tile[r][tv * VEC + q] = e[q];
+    }
+  }
+  __syncthreads();
+  // write: rows of the output (fixed x), 16-byte vectors along y
+  T *dst = out + out_off + y0 + (int64_t)tv * VEC;
+#pragma unroll
+  for (int c = tr; c < TILE; c += RPP) {
+    const int64_t x = x0 + c;
+    if (x < nx && y0 + tv * VEC < ny) {
+      uint4 v;
+      T *e = reinterpret_cast<T *>(&v);
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) e[q] = tile[tv * VEC + q][c];
+      __stcs(reinterpret_cast<uint4 *>(dst + x * out_sx), v);
+    }
+  }
+}
+
 // ---- row copy ---------------------------------------------------------------
 // Rows of length n along a dim that is inner in both tensors.
 template <typename T>
@@ -183,6 +229,21 @@ int launch_permute(const void *in, void *out, std::vector<Dim> dims, cudaStream_
   const int64_t tiles_x = (X.extent + TILE - 1) / TILE;
   const int64_t tiles_y = (Y.extent + TILE - 1) / TILE;
   const int64_t blocks = tiles_x * tiles_y * batch;
+  {
+    constexpr int64_t VEC = 16 / (int64_t)sizeof(T);
+    bool fast = X.in_stride == 1 && Y.out_stride == 1 && X.extent % VEC == 0 &&
+                Y.extent % VEC == 0 && Y.in_stride % VEC == 0 && X.out_stride % VEC == 0 &&
+                ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
+                tiles_x < 0x7fffffffLL && tiles_y < 65536 && batch < 65536;
+    for (int d = 0; d < bd.n && fast; ++d)
+      fast = bd.in_stride[d] % VEC == 0 && bd.out_stride[d] % VEC == 0;
+    if (fast) {
+      dim3 grid((unsigned)tiles_x, (unsigned)tiles_y, (unsigned)batch);
+      transpose_vec_kernel<T><<<grid, 256, 0, s>>>((const T *)in, (T *)out, X.extent, Y.extent,
+                                                    Y.in_stride, X.out_stride, bd);
+      return check_launch("permute transpose (vec)");
+    }
+  }
   if (blocks > 0x7fffffffLL) { set_error("bgx_permute: too many tiles"); return BGX_ERR_UNSUPPORTED; }
   dim3 block(32, BLK_Y);
   transpose_kernel<T><<<(unsigned)blocks, block, 0, s>>>(

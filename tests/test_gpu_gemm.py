@@ -198,3 +198,17 @@ def test_tile_choice_abi(dev):
         d.o_stride[:] = [0, N, 1]
         assert _lib.load().bgx_contract_tile(d, cg, bn) == 0
         assert cg.value in (1, 2) and bn.value in (64, 128, 256)
+
+
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("cta_group", [1, 2])
+def test_tcgen05_unaligned_output_uses_direct_stores(dev, out_dtype, cta_group):
+    """N = 100 (200-byte bf16 rows): no TMA map for the output, so the
+    epilogue falls back to direct stores; B is K-major so TC stays legal."""
+    a, b = rnd((200, 64), 51, dev, torch.bfloat16), rnd((100, 64), 52, dev, torch.bfloat16)
+    executor.reset_launch_log()
+    out = contract("(i,k),(j,k)->(i,j)", a, b, out_dtype=out_dtype, mode="tc",
+                   schedule={"cta_group": cta_group})
+    assert executor.launch_log() == ["tcgen05"]
+    want = oracle.gemm_kseq(np32(a), np.ascontiguousarray(np32(b).T))
+    assert oracle.rel_frobenius(np32(out), want) <= BF16_TOL
