@@ -66,22 +66,98 @@ def _contract_widened(spec, operands, c0, out, mode, schedule):
     return executor.run_gemm(plan, spec, list(operands), c0, out, mode=mode, schedule=schedule)
 
 
+def _row_streamable(spec: EinsumSpec, operands) -> bool:
+    """True when the output's leading index is the first operand's leading
+    index and appears in no other operand: output row slabs then depend only
+    on the matching row slab of operand 0 (the M-shard condition, §8e)."""
+    if not spec.output or not spec.inputs[0] or spec.inputs[0][0] != spec.output[0]:
+        return False
+    lead = spec.output[0]
+    return all(lead not in tup for tup in spec.inputs[1:])
+
+
 def contract_host(spec, *host_operands: torch.Tensor, out: torch.Tensor | None = None,
-                  device=None, **kw) -> torch.Tensor:
+                  device=None, chunk_rows: int | None = None, **kw) -> torch.Tensor:
     """Host-buffer form of ``contract`` (what a numpy/CPU caller of the
-    reference API pays for): copies the operands host→device on the current
-    stream (async when they are pinned), runs the contraction on the device,
-    and copies the result back into ``out`` (a host tensor; pinned for an
-    async copy) or a fresh host tensor.  Synchronises before returning."""
+    reference API pays for): operands are copied host→device, contracted on
+    the device, and the result copied back into ``out`` (pinned host tensor)
+    or a fresh pinned tensor.  Synchronises before returning.
+
+    When the spec is row-streamable (output rows depend only on the same rows
+    of operand 0 — e.g. the BASELINE chain and plain GEMMs) and the host
+    buffers are pinned, the work is pipelined over row chunks on three
+    streams: H2D of chunk i+1 and D2H of chunk i-1 overlap the contraction of
+    chunk i (PCIe is full duplex), so the call costs ~max(H2D, compute, D2H)
+    instead of their sum.  Results are identical to the unchunked call (row
+    slabs are independent; every kernel's per-row arithmetic is unchanged)."""
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
     device = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
-    dev_ops = [t.to(device, non_blocking=True) for t in host_operands]
     c0 = kw.pop("c0", None)
-    if c0 is not None:
-        c0 = c0.to(device, non_blocking=True)
-    res = contract(spec, *dev_ops, c0=c0, **kw)
+    out_shape = output_shape(spec, host_operands)
+    rows = out_shape[0] if out_shape else 0
+    pinned = all(t.is_pinned() for t in host_operands) and (c0 is None or c0.is_pinned())
+    if chunk_rows is None:
+        chunk_rows = 2048
+    stream_ok = (_row_streamable(spec, host_operands) and pinned and rows > chunk_rows
+                 and (out is None or out.is_pinned()))
+    if not stream_ok:
+        dev_ops = [t.to(device, non_blocking=True) for t in host_operands]
+        dev_c0 = c0.to(device, non_blocking=True) if c0 is not None else None
+        res = contract(spec, *dev_ops, c0=dev_c0, **kw)
+        if out is None:
+            out = torch.empty(res.shape, dtype=res.dtype, pin_memory=True)
+        out.copy_(res, non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()
+        return out
+    dt = kw.get("out_dtype") or host_operands[0].dtype
     if out is None:
-        out = torch.empty(res.shape, dtype=res.dtype, pin_memory=True)
-    out.copy_(res, non_blocking=True)
-    torch.cuda.current_stream(device).synchronize()
+        out = torch.empty(out_shape, dtype=dt, pin_memory=True)
+    comp = torch.cuda.current_stream(device)
+    h2d = torch.cuda.Stream(device)
+    d2h = torch.cuda.Stream(device)
+    a = host_operands[0]
+    with torch.cuda.stream(h2d):
+        others = [t.to(device, non_blocking=True) for t in host_operands[1:]]
+    for t in others:
+        t.record_stream(comp)
+    others_ready = torch.cuda.Event()
+    others_ready.record(h2d)
+    n_chunks = (rows + chunk_rows - 1) // chunk_rows
+    nbuf = 2
+    a_buf = [torch.empty((chunk_rows, *a.shape[1:]), dtype=a.dtype, device=device)
+             for _ in range(nbuf)]
+    o_buf = [torch.empty((chunk_rows, *out_shape[1:]), dtype=dt, device=device)
+             for _ in range(nbuf)]
+    c_buf = ([torch.empty((chunk_rows, *out_shape[1:]), dtype=c0.dtype, device=device)
+              for _ in range(nbuf)] if c0 is not None else None)
+    ev_h2d = [torch.cuda.Event() for _ in range(n_chunks)]
+    ev_comp = [torch.cuda.Event() for _ in range(n_chunks)]
+    ev_d2h = [torch.cuda.Event() for _ in range(n_chunks)]
+    for i in range(n_chunks):
+        r0, r1 = i * chunk_rows, min(rows, (i + 1) * chunk_rows)
+        n = r1 - r0
+        slot = i % nbuf
+        with torch.cuda.stream(h2d):
+            if i >= nbuf:
+                h2d.wait_event(ev_comp[i - nbuf])       # input slot consumed
+            a_buf[slot][:n].copy_(a[r0:r1], non_blocking=True)
+            if c_buf is not None:
+                c_buf[slot][:n].copy_(c0[r0:r1], non_blocking=True)
+            ev_h2d[i].record(h2d)
+        comp.wait_event(ev_h2d[i])
+        if i == 0:
+            comp.wait_event(others_ready)
+        if i >= nbuf:
+            comp.wait_event(ev_d2h[i - nbuf])            # output slot drained
+        contract(spec, a_buf[slot][:n], *others, out=o_buf[slot][:n],
+                 c0=c_buf[slot][:n] if c_buf is not None else None, **kw)
+        ev_comp[i].record(comp)
+        with torch.cuda.stream(d2h):
+            d2h.wait_event(ev_comp[i])
+            out[r0:r1].copy_(o_buf[slot][:n], non_blocking=True)
+            ev_d2h[i].record(d2h)
+    d2h.synchronize()
+    comp.synchronize()
     return out

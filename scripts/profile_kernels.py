@@ -13,9 +13,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--what", default="gemm4096,chain_gemm,perm8192")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile-n", type=int, default=0)
+ap.add_argument("--rasters", default="0")
+ap.add_argument("--cg", type=int, default=0)
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 sched = {"tile_n": args.tile_n} if args.tile_n else None
+if args.cg:
+    sched = dict(sched or {}, cta_group=args.cg)
 for what in args.what.split(","):
     if what == "gemm4096":
         a = torch.randn(4096, 4096, device=dev).bfloat16()
@@ -25,8 +29,10 @@ for what in args.what.split(","):
     elif what == "chain_gemm":
         a = torch.randn(32768, 8192, device=dev).bfloat16()
         b = torch.randn(8192, 8192, device=dev).bfloat16()
-        for _ in range(args.reps):
-            contract("(i,k),(k,j)->(i,j)", a, b, schedule=sched)
+        for ra in (int(x) for x in args.rasters.split(",")):
+            sc = dict(sched or {}, raster=ra) if ra else sched
+            for _ in range(args.reps):
+                contract("(i,k),(k,j)->(i,j)", a, b, schedule=sc)
     elif what == "batched":
         a = torch.randn(64, 1024, 1024, device=dev).bfloat16()
         b = torch.randn(64, 1024, 1024, device=dev).bfloat16()
