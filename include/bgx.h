@@ -125,11 +125,13 @@ typedef enum {
 } bgx_mode;
 
 typedef struct {
-  int32_t tile_n;     /* 0 = auto; TC: 64/128/256                           */
+  int32_t tile_n;     /* 0 = auto; TC: 64/128/256, 512 (CTA pair only: two
+                         N=256 MMAs per K-step, single TMEM accumulator)      */
   int32_t stages;     /* 0 = auto; TC smem pipeline depth                   */
   int32_t cta_group;  /* 0 = auto; TC: 1 or 2 (CTA pair, M = 256)           */
   int32_t max_ctas;   /* 0 = auto (persistent: one CTA per SM)              */
-  int32_t raster;     /* 0 = auto; L2 tile-group width along M              */
+  int32_t raster;     /* 0 = auto; >0: groups of this many M-tiles (A slab
+                         L2-resident), <0: groups of |raster| N-tiles         */
   int32_t reserved[3]; /* reserved[0] bit 0: skip epilogue stores (timing
                           probe only — the output is NOT written)            */
 } bgx_schedule;

@@ -41,7 +41,8 @@ namespace {
 constexpr int BM = 128;                     // rows of A per CTA
 constexpr int BK = 64;                      // 64 x 16-bit = 128 B = one swizzle row
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
-constexpr int NUM_THREADS = 256;
+constexpr int EPI_WARPS = 8;                // 2 warps per TMEM lane quadrant
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int SMEM_BUDGET = 227 * 1024;
 
 struct TcParams {
@@ -59,14 +60,21 @@ struct TcParams {
 
 template <int BN, int CG, int OUT_BYTES> struct Cfg {
   static constexpr int BN_CTA = BN / CG;                 // B columns staged per CTA
+  // one tcgen05.mma covers at most N = 256: wider tiles issue NSPLIT MMAs per
+  // K-step into adjacent TMEM column ranges
+  static constexpr int MMA_N = BN > 256 ? 256 : BN;
+  static constexpr int NSPLIT = BN / MMA_N;
+  static constexpr int B_BOX_N = MMA_N / CG;             // B columns per CTA per MMA
+  static constexpr int B_HALF_BYTES = B_BOX_N * BK * 2;
   static constexpr int B_STAGE_BYTES = BN_CTA * BK * 2;
+  static constexpr int ACC_BUFS = 2 * BN <= 512 ? 2 : 1; // double-buffered accumulator?
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols) of the output
   static constexpr int EPI_BUF_BYTES = 32 * 32 * OUT_BYTES;
-  static constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BUF_BYTES;
   static constexpr int STAGES_RAW = (SMEM_BUDGET - 2048 - EPI_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int TMEM_COLS = ACC_BUFS * BN < 32 ? 32 : ACC_BUFS * BN;
   static constexpr int SMEM_BYTES =
       STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr int TILE_M = BM * CG;
@@ -77,13 +85,26 @@ __device__ __forceinline__ void tile_coords(const TcParams &p, int64_t t, int64_
   const int64_t per_batch = (int64_t)p.tiles_m * p.tiles_n;
   b = t / per_batch;
   int64_t r = t % per_batch;
-  const int64_t G = p.raster;
-  const int64_t group = r / (G * p.tiles_n);
-  const int64_t in_group = r % (G * p.tiles_n);
-  const int64_t first_m = group * G;
-  const int64_t gm = (p.tiles_m - first_m) < G ? (p.tiles_m - first_m) : G;
-  tm = first_m + in_group % gm;
-  tn = in_group / gm;
+  if (p.raster > 0) {
+    // groups of G M-tiles; inside a group M fastest, then N (A slab resident)
+    const int64_t G = p.raster;
+    const int64_t group = r / (G * p.tiles_n);
+    const int64_t in_group = r % (G * p.tiles_n);
+    const int64_t first_m = group * G;
+    const int64_t gm = (p.tiles_m - first_m) < G ? (p.tiles_m - first_m) : G;
+    tm = first_m + in_group % gm;
+    tn = in_group / gm;
+  } else {
+    // groups of G N-tiles; inside a group N fastest, then M (B slab resident
+    // in L2 while A streams through once per group)
+    const int64_t G = -p.raster;
+    const int64_t group = r / (G * p.tiles_m);
+    const int64_t in_group = r % (G * p.tiles_m);
+    const int64_t first_n = group * G;
+    const int64_t gn = (p.tiles_n - first_n) < G ? (p.tiles_n - first_n) : G;
+    tn = first_n + in_group % gn;
+    tm = in_group / gn;
+  }
 }
 
 // Write one thread's row of 32 output values into the warp's swizzled staging
@@ -194,7 +215,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 4 * CG);  // one arrive per epilogue warp per CTA
+      mbar_init(&tmem_empty[a], EPI_WARPS * CG);  // one arrive per epilogue warp per CTA
     }
     fence_barrier_init();
   }
@@ -210,13 +231,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   if (warp == 0) {
     // ===== TMA producer (every CTA loads its own A rows / B columns) =====
     // Warp-uniform loop; one elected lane issues the barrier ops and copies.
+    // Clusters start staggered (a few hundred ns apart) so that the epilogue
+    // store bursts of different SMs do not coincide: with equal tile times the
+    // offset persists for the whole persistent loop.
+    if (C::ACC_BUFS == 1 && !(p.debug & 8)) {
+      const unsigned delay = (unsigned)(cluster_id % 16) * 256u;
+      if (delay) __nanosleep(delay);
+    }
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
       const int32_t m0 = (int32_t)(tm * C::TILE_M + rank * BM);
-      const int32_t n0 = (int32_t)(tn * BN + rank * BN_CTA);
+      // B columns of this CTA: for each MMA split h, [h*MMA_N + rank*B_BOX_N, +B_BOX_N)
+      const int32_t n0 = (int32_t)(tn * BN + rank * C::B_BOX_N);
       const int32_t bb = (int32_t)b;
       for (int kb = 0; kb < p.k_blocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
@@ -231,12 +260,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           } else {
             tma_load<CG>(sa, &tmap_a, &full[stage], k0, m0, bb);
           }
-          if (p.b_mn) {
 #pragma unroll
-            for (int j = 0; j < BN_CTA / 64; ++j)
-              tma_load<CG>(sb + j * 8192, &tmap_b, &full[stage], n0 + 64 * j, k0, bb);
-          } else {
-            tma_load<CG>(sb, &tmap_b, &full[stage], k0, n0, bb);
+          for (int h = 0; h < C::NSPLIT; ++h) {
+            uint8_t *sbh = sb + h * C::B_HALF_BYTES;
+            const int32_t nh = n0 + h * C::MMA_N;
+            if (p.b_mn) {
+#pragma unroll
+              for (int j = 0; j < C::B_BOX_N / 64; ++j)
+                tma_load<CG>(sbh + j * 8192, &tmap_b, &full[stage], nh + 64 * j, k0, bb);
+            } else {
+              tma_load<CG>(sbh, &tmap_b, &full[stage], k0, nh, bb);
+            }
           }
         }
         __syncwarp();
@@ -255,23 +289,68 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const uint64_t a_fixed = make_sdesc_sw128(0, p.a_mn ? 8192u : 16u, 1024);
       const uint64_t b_fixed = make_sdesc_sw128(0, p.b_mn ? 8192u : 16u, 1024);
       const uint32_t sa0 = smem_u32(smem_a) >> 4, sb0 = smem_u32(smem_b) >> 4;
+      // With a single 512-column accumulator (BN = 512) the two N = 256 halves
+      // are released separately by the epilogue (tmem_empty[0] = columns
+      // [0,256), tmem_empty[1] = [256,512)): the next tile's first-half MMAs
+      // run over every resident stage while the second half still drains.
+      constexpr bool SPLIT_RELEASE = C::ACC_BUFS == 1 && C::NSPLIT == 2;
+      auto issue = [&](int st, int kb, int h_lo, int h_hi, uint32_t d_tmem) {
+        const uint64_t ad0 = a_fixed | (uint64_t)(sa0 + st * (A_STAGE_BYTES >> 4));
+        const uint64_t bd0 = b_fixed | (uint64_t)(sb0 + st * (C::B_STAGE_BYTES >> 4));
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+#pragma unroll
+          for (int h = 0; h < C::NSPLIT; ++h)
+            if (h >= h_lo && h < h_hi)
+              umma_f16<CG>(d_tmem + h * C::MMA_N, ad0 + k * a_step,
+                           bd0 + h * (C::B_HALF_BYTES >> 4) + k * b_step, p.idesc,
+                           (kb | k) != 0);
+      };
+      auto release = [&](int st) {
+        if constexpr (CG == 1) umma_commit(&empty[st]);
+        else umma_commit_mc(&empty[st], 0x3);
+      };
       for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
-        tc_fence_after();
+        const int acc = it % C::ACC_BUFS;
+        const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.k_blocks; ++kb) {
+        int kb = 0;
+        if constexpr (SPLIT_RELEASE) {
+          const int early = p.k_blocks < STAGES ? p.k_blocks : STAGES;
+          const int stage0 = stage;
+          const uint32_t phase0 = phase;
+          mbar_wait(&tmem_empty[0], acc_phase ^ 1);
+          tc_fence_after();
+          for (int e = 0; e < early; ++e) {          // first half, resident stages
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one()) issue(stage, e, 0, 1, d_tmem);
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          mbar_wait(&tmem_empty[1], acc_phase ^ 1);
+          tc_fence_after();
+          stage = stage0;
+          phase = phase0;
+          for (int e = 0; e < early; ++e) {          // second half, same stages
+            if (elect_one()) {
+              issue(stage, e, 1, 2, d_tmem);
+              release(stage);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          kb = early;
+        } else {
+          mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+          tc_fence_after();
+        }
+        for (; kb < p.k_blocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
-            const uint64_t ad0 = a_fixed | (uint64_t)(sa0 + stage * (A_STAGE_BYTES >> 4));
-            const uint64_t bd0 = b_fixed | (uint64_t)(sb0 + stage * (C::B_STAGE_BYTES >> 4));
-#pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma_f16<CG>(d_tmem, ad0 + k * a_step, bd0 + k * b_step, p.idesc, (kb | k) != 0);
-            if constexpr (CG == 1) umma_commit(&empty[stage]);
-            else umma_commit_mc(&empty[stage], 0x3);
+            issue(stage, kb, 0, C::NSPLIT, d_tmem);
+            release(stage);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -285,26 +364,103 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
   } else if (warp >= 4) {
     // ===== epilogue (every CTA drains its own 128 TMEM lanes) =====
-    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
+    // 8 warps: warp w reads TMEM lane quadrant w % 4 (hardware rule) and the
+    // column chunks c = g, g + 2, ... of it (g = which of the two warps on that
+    // quadrant); the next chunk's tcgen05.ld is in flight while the current
+    // one is converted, staged and stored.
+    const int ew = warp - 4;
+    const int quad = warp % 4;  // TMEM lanes [32*quad, 32*quad + 32)
+    const int g = ew / 4;
     uint8_t *ebuf = smem_epi + ew * 2 * C::EPI_BUF_BYTES;
     int it = 0, chunk = 0;
     for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = it % C::ACC_BUFS;
+      const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const int64_t m_warp = tm * C::TILE_M + rank * BM + ew * 32;
+      constexpr bool SPLIT_RELEASE = C::ACC_BUFS == 1 && C::NSPLIT == 2;
+      auto arrive_empty = [&](int which) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) mbar_arrive(&tmem_empty[which]);
+          else mbar_arrive_cluster(&tmem_empty[which], 0);
+        }
+      };
+      if (p.debug & 4) {  // timing probe: release the accumulator without reading it
+        arrive_empty(acc);
+        if (SPLIT_RELEASE) arrive_empty(1);
+        continue;
+      }
+      const int64_t m_warp = tm * C::TILE_M + rank * BM + quad * 32;
       const int64_t m = m_warp + lane;
       const bool row_ok = m < p.M;
       OutT *orow = static_cast<OutT *>(p.out) + b * p.so[0] + m * p.so[1];
       const OutT *crow = p.c0 ? static_cast<const OutT *>(p.c0) + b * p.sc[0] + m * p.sc[1] : nullptr;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      constexpr int NCHUNK = BN / 32;
+      if constexpr (SPLIT_RELEASE && sizeof(OutT) == 2) {
+        if (p.tma_store && crow == nullptr && !(p.debug & 1)) {
+          // Two-phase drain: read this warp's chunks of each accumulator half
+          // into packed 16-bit registers, release that half of TMEM to the MMA
+          // warp, and only then stage + TMA-store — the stores (and their
+          // buffer waits) leave the MMA critical path.
+          constexpr int PER_HALF = NCHUNK / 2 / 2;  // chunks per warp per half
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c * 32, r);
+          for (int half = 0; half < 2; ++half) {
+            uint32_t pk[PER_HALF][16];
+#pragma unroll
+            for (int j = 0; j < PER_HALF; ++j) {
+              const int c = half * (NCHUNK / 2) + g + 2 * j;
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(taddr + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int q = 0; q < 16; ++q) {
+                OutT lo = Conv<OutT>::from_f(__uint_as_float(r[2 * q]));
+                OutT hi = Conv<OutT>::from_f(__uint_as_float(r[2 * q + 1]));
+                pk[j][q] = (uint32_t)(*reinterpret_cast<uint16_t *>(&lo)) |
+                           ((uint32_t)(*reinterpret_cast<uint16_t *>(&hi)) << 16);
+              }
+            }
+            arrive_empty(half);   // this half of TMEM is free for the next tile
+#pragma unroll
+            for (int j = 0; j < PER_HALF; ++j) {
+              const int c = half * (NCHUNK / 2) + g + 2 * j;
+              const int64_t n = tn * BN + c * 32;
+              if (n >= p.N) continue;
+              uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
+              ++chunk;
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+#pragma unroll
+              for (int v4 = 0; v4 < 4; ++v4) {
+                uint4 w = make_uint4(pk[j][4 * v4], pk[j][4 * v4 + 1], pk[j][4 * v4 + 2],
+                                     pk[j][4 * v4 + 3]);
+                *reinterpret_cast<uint4 *>(buf + lane * 64 + ((v4 ^ ((lane >> 1) & 3)) << 4)) = w;
+              }
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&tmap_o, buf, (int32_t)n, (int32_t)m_warp, (int32_t)b);
+                bulk_commit();
+              }
+            }
+          }
+          continue;
+        }
+      }
+      uint32_t rbuf[2][32];
+      tmem_ld_32x32b_x32(taddr + g * 32, rbuf[0]);
+#pragma unroll 2
+      for (int c = g, k = 0; c < NCHUNK; c += 2, ++k) {
         tmem_ld_wait();
+        uint32_t (&r)[32] = rbuf[k & 1];
+        if (SPLIT_RELEASE && c >= NCHUNK / 2 && c - 2 < NCHUNK / 2)
+          arrive_empty(0);  // every chunk of columns [0, BN/2) has been read
+        if (c + 2 < NCHUNK) tmem_ld_32x32b_x32(taddr + (c + 2) * 32, rbuf[(k + 1) & 1]);
         const int64_t n = tn * BN + c * 32;
         if (n >= p.N || (p.debug & 1)) continue;  // warp-uniform
         float v[32];
@@ -331,12 +487,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           Store<OutT>::row32(orow + n, v, valid >= 32, valid);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 1) mbar_arrive(&tmem_empty[acc]);
-        else mbar_arrive_cluster(&tmem_empty[acc], 0);
-      }
+      tmem_ld_wait();
+      arrive_empty(SPLIT_RELEASE ? 1 : acc);
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
@@ -428,7 +580,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   if (p.b_mn)
     rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], 64, 64);
   else
-    rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], 64, C::BN_CTA);
+    rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], 64, C::B_BOX_N);
   if (rc) return rc;
   // output map for the TMA-store epilogue (falls back to direct stores when
   // the output's row/batch strides are not 16-byte multiples)
@@ -445,7 +597,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
                   oes == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
-  p.idesc = make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, BN);
+  p.idesc = make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, C::MMA_N);
   p.stages = (d.sched.stages >= 2 && d.sched.stages <= C::STAGES) ? d.sched.stages : C::STAGES;
   p.tiles_m = (int32_t)((d.M + C::TILE_M - 1) / C::TILE_M);
   p.tiles_n = (int32_t)((d.N + BN - 1) / BN);
@@ -487,6 +639,7 @@ int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStrea
   switch (bn) {
     case 64: return CG == 1 ? launch_tc<64, 1, OutT>(d, p, s) : launch_tc<128, CG, OutT>(d, p, s);
     case 128: return launch_tc<128, CG, OutT>(d, p, s);
+    case 512: return CG == 2 ? launch_tc<512, 2, OutT>(d, p, s) : launch_tc<256, CG, OutT>(d, p, s);
     default: return launch_tc<256, CG, OutT>(d, p, s);
   }
 }
@@ -499,8 +652,8 @@ int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStrea
 // L2->SM bytes of B).  A later candidate must be >3 % cheaper to win.
 void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
   struct Cand { int cg, bn; double eff; };
-  const Cand cands[] = {{2, 256, 1.00}, {2, 128, 0.85}, {1, 256, 0.88}, {1, 128, 0.80},
-                        {1, 64, 0.60}};
+  const Cand cands[] = {{2, 512, 1.06}, {2, 256, 1.00}, {2, 128, 0.85}, {1, 256, 0.88},
+                        {1, 128, 0.80}, {1, 64, 0.60}};
   double best = -1.0;
   for (const Cand &c : cands) {
     if (c.bn > 64 && d.N <= c.bn / 2) continue;  // tiles would be mostly empty
@@ -509,6 +662,9 @@ void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
     const int64_t slots = sms / c.cg;
     const int64_t waves = (tm * tn * d.batch + slots - 1) / slots;
     const double cost = (double)waves * (double)(128 * c.bn) / c.eff;
+    // single 512-column accumulator: its drain is amortised only over long K
+    // and many waves (4096^3 measured faster with 256-wide tiles)
+    if (c.bn == 512 && (d.N < 1024 || d.K < 8192 || waves < 8)) continue;
     if (best < 0 || cost < best * 0.97) {
       best = cost;
       cg = c.cg;
@@ -560,7 +716,9 @@ int contract_tc(const bgx_contract_desc &d, cudaStream_t s) {
   for (int i = 0; i < 3; ++i) { p.sc[i] = d.c_stride[i]; p.so[i] = d.o_stride[i]; }
   int cg = 0, bn = 0;
   tc_tile_choice(d, &cg, &bn);
-  p.raster = d.sched.raster > 0 ? d.sched.raster : (cg == 2 ? 8 : 16);
+  // default raster: 512-wide pair tiles keep an 8-N-tile slab of B (8 x 512
+  // columns) L2-resident while A streams (-8); otherwise M-groups.
+  p.raster = d.sched.raster != 0 ? d.sched.raster : (bn == 512 ? -8 : (cg == 2 ? 8 : 16));
   p.debug = d.sched.reserved[0];
   if (d.out_dtype == BGX_F32)
     return cg == 2 ? dispatch_bn<2, float>(d, bn, p, s) : dispatch_bn<1, float>(d, bn, p, s);
@@ -575,8 +733,11 @@ void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out) {
   int cg = 0, bn = 0;
   choose_tile(d, sm_count_current(), cg, bn);
   if (d.sched.cta_group == 1 || d.sched.cta_group == 2) cg = d.sched.cta_group;
-  if (d.sched.tile_n == 64 || d.sched.tile_n == 128 || d.sched.tile_n == 256) bn = d.sched.tile_n;
+  if (d.sched.tile_n == 64 || d.sched.tile_n == 128 || d.sched.tile_n == 256 ||
+      d.sched.tile_n == 512)
+    bn = d.sched.tile_n;
   if (cg == 2 && bn == 64) bn = 128;
+  if (cg == 1 && bn == 512) bn = 256;
   *cg_out = cg;
   *bn_out = bn;
 }

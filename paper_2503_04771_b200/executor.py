@@ -137,7 +137,11 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
     d.mode = MODES[mode]
     if schedule:
         for k, v in schedule.items():
-            setattr(d.sched, k, int(v))
+            if k == "reserved":
+                for i, x in enumerate(v):
+                    d.sched.reserved[i] = int(x)
+            else:
+                setattr(d.sched, k, int(v))
     kind = lib.bgx_contract_kernel(d)
     _lib.check(kind if kind < 0 else 0, "bgx_contract_kernel")
     with torch.cuda.device(out.device):

@@ -15,6 +15,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tile-n", type=int, default=0)
 ap.add_argument("--rasters", default="0")
 ap.add_argument("--cg", type=int, default=0)
+ap.add_argument("--debugs", default="0")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 sched = {"tile_n": args.tile_n} if args.tile_n else None
@@ -30,9 +31,14 @@ for what in args.what.split(","):
         a = torch.randn(32768, 8192, device=dev).bfloat16()
         b = torch.randn(8192, 8192, device=dev).bfloat16()
         for ra in (int(x) for x in args.rasters.split(",")):
-            sc = dict(sched or {}, raster=ra) if ra else sched
-            for _ in range(args.reps):
-                contract("(i,k),(k,j)->(i,j)", a, b, schedule=sc)
+            for dbg in (int(x) for x in args.debugs.split(",")):
+                sc = dict(sched or {})
+                if ra:
+                    sc["raster"] = ra
+                if dbg:
+                    sc["reserved"] = [dbg, 0, 0]
+                for _ in range(args.reps):
+                    contract("(i,k),(k,j)->(i,j)", a, b, schedule=sc or None)
     elif what == "batched":
         a = torch.randn(64, 1024, 1024, device=dev).bfloat16()
         b = torch.randn(64, 1024, 1024, device=dev).bfloat16()

@@ -94,15 +94,15 @@ LAYOUTS = {
 @pytest.mark.parametrize("layout", list(LAYOUTS))
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 640), (200, 136, 72), (1000, 520, 1000)])
-@pytest.mark.parametrize("cta_group", [1, 2])
-def test_tcgen05_layouts(dev, layout, dtype, M, N, K, cta_group):
+@pytest.mark.parametrize("cta_group,tile_n", [(1, 0), (2, 0), (2, 512)])
+def test_tcgen05_layouts(dev, layout, dtype, M, N, K, cta_group, tile_n):
     spec = E.parse_einsum(LAYOUTS[layout])
     shp = {"i": M, "j": N, "k": K}
     a = rnd(tuple(shp[x] for x in spec.inputs[0]), 11, dev, dtype)
     b = rnd(tuple(shp[x] for x in spec.inputs[1]), 12, dev, dtype)
     executor.reset_launch_log()
     out = contract(spec, a, b, out_dtype=torch.float32, mode="tc",
-                   schedule={"cta_group": cta_group})
+                   schedule={"cta_group": cta_group, "tile_n": tile_n})
     assert executor.launch_log() == ["tcgen05"]
     A = np32(a) if spec.inputs[0] == ("i", "k") else np32(a).T
     B = np32(b) if spec.inputs[1] == ("k", "j") else np32(b).T
@@ -113,11 +113,11 @@ def test_tcgen05_layouts(dev, layout, dtype, M, N, K, cta_group):
     assert err <= 1e-5, err
 
 
-@pytest.mark.parametrize("tile_n", [64, 128, 256])
+@pytest.mark.parametrize("tile_n", [64, 128, 256, 512])
 @pytest.mark.parametrize("cta_group", [1, 2])
 def test_tcgen05_tile_sizes_and_bf16_out(dev, tile_n, cta_group):
-    a, b = rnd((384, 320), 21, dev, torch.bfloat16), rnd((320, 448), 22, dev, torch.bfloat16)
-    c0 = rnd((384, 448), 23, dev, torch.bfloat16)
+    a, b = rnd((384, 320), 21, dev, torch.bfloat16), rnd((320, 1088), 22, dev, torch.bfloat16)
+    c0 = rnd((384, 1088), 23, dev, torch.bfloat16)
     out = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="tc",
                    schedule={"tile_n": tile_n, "cta_group": cta_group})
     assert out.dtype == torch.bfloat16
@@ -197,7 +197,7 @@ def test_tile_choice_abi(dev):
         d.b_stride[:] = [0, N, 1]
         d.o_stride[:] = [0, N, 1]
         assert _lib.load().bgx_contract_tile(d, cg, bn) == 0
-        assert cg.value in (1, 2) and bn.value in (64, 128, 256)
+        assert cg.value in (1, 2) and bn.value in (64, 128, 256, 512)
 
 
 @pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
