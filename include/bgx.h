@@ -163,6 +163,18 @@ BGX_API int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group, in
 BGX_API int bgx_cast_f32(const float *src, const void *c0, void *out, int32_t out_dtype,
                  int64_t n, void *stream);
 
+/* ---- runtime-compiled kernels (GPU case study) ---------
+ * Replaces the simulated sequential thread grid of bridgegen run_kernel
+ * (interp.py:434-461): CUDA C generated from an IR kernel is compiled with
+ * NVRTC for sm_100a (no FMA contraction, no FTZ) and launched as a 1-D grid of
+ * `grid` blocks x `block` threads; `args` is the cudaLaunchKernel argument
+ * array.  `log` (optional) receives the compiler log.                      */
+BGX_API int bgx_rtc_compile(const char *src, const char *name, void **handle, char *log,
+                            int64_t log_len);
+BGX_API int bgx_rtc_launch(void *handle, uint64_t grid, uint32_t block, void **args,
+                           void *stream);
+BGX_API int bgx_rtc_free(void *handle);
+
 #ifdef __cplusplus
 }
 #endif

@@ -128,19 +128,27 @@ def _generic_b200(self, op, env):
     return None
 
 
-def install(mode: str = "auto") -> None:
+def install(mode: str = "auto", kernels: bool = True) -> None:
     """Route ``bridgegen.interp._Machine._generic`` to libbgx.so.  ``mode``:
-    'auto' (bit-exact for f32/f64), 'exact', 'ffma', 'tc', 'simt'."""
+    'auto' (bit-exact for f32/f64), 'exact', 'ffma', 'tc', 'simt'.  With
+    ``kernels`` also replace ``interp.run_kernel`` (the simulated thread grid,
+    interp.py:434-461) by real NVRTC-compiled launches (fir_gpu.run_kernel)."""
+    from . import fir_gpu
     interp = _interp_module()
     if "orig" not in _saved:
         _saved["orig"] = interp._Machine._generic
+        _saved["orig_run_kernel"] = interp.run_kernel
     _saved["mode"] = mode
     interp._Machine._generic = _generic_b200
+    if kernels:
+        interp.run_kernel = fir_gpu.run_kernel
 
 
 def uninstall() -> None:
     if "orig" in _saved:
-        _interp_module()._Machine._generic = _saved.pop("orig")
+        interp = _interp_module()
+        interp._Machine._generic = _saved.pop("orig")
+        interp.run_kernel = _saved.pop("orig_run_kernel")
 
 
 def installed() -> bool:
