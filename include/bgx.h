@@ -157,6 +157,18 @@ BGX_API int bgx_contract_kernel(const bgx_contract_desc *d);
  * descriptor would not run on tensor cores. */
 BGX_API int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group, int32_t *tile_n);
 
+/* ---- split-K on one GPU --------------------------------------------------
+ * For contractions whose batch x M x N tiles leave most SMs idle (small
+ * output, long K): `splits` persistent units per tile each contract a K slice
+ * on the tensor cores into f32 partials in `workspace` (splits x batch x M x N
+ * floats), then one reduction kernel sums the slices in order, adds c0 and
+ * casts.  bgx_contract_splitk_plan returns the split count the library would
+ * use (1 = not worth it) and the workspace size in bytes.                  */
+BGX_API int bgx_contract_splitk_plan(const bgx_contract_desc *d, int32_t *splits,
+                                     int64_t *workspace_bytes);
+BGX_API int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, void *workspace,
+                                int64_t workspace_bytes, void *stream);
+
 /* ---- elementwise helpers for multi-GPU K-split -------------------------
  * out[i] = (dtype_out) src[i] for n elements, src f32 (the reduced partials),
  * out f32/bf16/f16; with c0 != NULL adds c0[i] first (in f32).           */

@@ -74,6 +74,10 @@ SIGNATURES = {
     "bgx_contract_kernel": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc)]),
     "bgx_contract_tile": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
                                          ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "bgx_contract_splitk_plan": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
+                                                ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
+    "bgx_contract_splitk": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc), _i32, _vp, _i64,
+                                           _vp]),
     "bgx_cast_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _vp]),
     "bgx_rtc_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p,
                                        ctypes.POINTER(_vp), ctypes.c_char_p, _i64]),

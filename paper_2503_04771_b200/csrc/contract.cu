@@ -6,6 +6,9 @@ bool tc_legal(const bgx_contract_desc &d, const char **why);
 int contract_tc(const bgx_contract_desc &d, cudaStream_t s);
 int contract_simt(const bgx_contract_desc &d, int kind, cudaStream_t s);
 void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out);
+void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes);
+int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t ws_bytes,
+                       cudaStream_t s);
 
 namespace {
 
@@ -102,4 +105,34 @@ extern "C" int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group,
   *cta_group = cg;
   *tile_n = bn;
   return BGX_OK;
+}
+
+extern "C" int bgx_contract_splitk_plan(const bgx_contract_desc *d, int32_t *splits,
+                                        int64_t *workspace_bytes) {
+  BGX_CHECK_ARG(d && splits && workspace_bytes, "bgx_contract_splitk_plan: null argument");
+  int rc = validate(*d);
+  if (rc) return rc;
+  int sp = 1;
+  int64_t ws = 0;
+  if (select_kind(*d) == KIND_TC) tc_splitk_plan(*d, &sp, &ws);
+  *splits = sp;
+  *workspace_bytes = ws;
+  return BGX_OK;
+}
+
+extern "C" int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, void *workspace,
+                                   int64_t workspace_bytes, void *stream) {
+  BGX_CHECK_ARG(d != nullptr, "bgx_contract_splitk: null descriptor");
+  int rc = validate(*d);
+  if (rc) return rc;
+  if (d->batch == 0 || d->M == 0 || d->N == 0) return BGX_OK;
+  if (splits <= 1 || d->K == 0) return bgx_contract(d, stream);
+  const int kind = select_kind(*d);
+  if (kind != KIND_TC) {
+    set_error("bgx_contract_splitk: split-K runs on the tensor-core path only");
+    return kind < 0 ? kind : BGX_ERR_UNSUPPORTED;
+  }
+  BGX_CHECK_ARG(d->a != nullptr && d->b != nullptr && d->out != nullptr,
+                "bgx_contract_splitk: null operand");
+  return contract_tc_splitk(*d, splits, workspace, workspace_bytes, (cudaStream_t)stream);
 }

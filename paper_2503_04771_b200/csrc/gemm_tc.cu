@@ -49,6 +49,8 @@ struct TcParams {
   int64_t batch, M, N, K;
   int32_t tiles_m, tiles_n, k_blocks, raster;
   int64_t num_tiles;
+  int32_t k_splits, kb_per_split;  // split-K: unit u -> tile u % num_tiles, K slice u / num_tiles
+  int64_t num_units;
   uint32_t idesc;
   int32_t a_mn, b_mn;            // 1 = MN-major operand
   int32_t stages;                // ring depth actually used (<= Cfg::STAGES)
@@ -240,14 +242,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
     int stage = 0;
     uint32_t phase = 0;
-    for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters) {
+    for (int64_t u = cluster_id; u < p.num_units; u += num_clusters) {
+      const int64_t t = u % p.num_tiles;
+      const int kb_lo = (int)(u / p.num_tiles) * p.kb_per_split;
+      const int kb_hi = kb_lo + p.kb_per_split < p.k_blocks ? kb_lo + p.kb_per_split : p.k_blocks;
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
       const int32_t m0 = (int32_t)(tm * C::TILE_M + rank * BM);
       // B columns of this CTA: for each MMA split h, [h*MMA_N + rank*B_BOX_N, +B_BOX_N)
       const int32_t n0 = (int32_t)(tn * BN + rank * C::B_BOX_N);
       const int32_t bb = (int32_t)b;
-      for (int kb = 0; kb < p.k_blocks; ++kb) {
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
           if (leader) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
@@ -310,13 +315,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         if constexpr (CG == 1) umma_commit(&empty[st]);
         else umma_commit_mc(&empty[st], 0x3);
       };
-      for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+      for (int64_t u = cluster_id; u < p.num_units; u += num_clusters, ++it) {
+        const int kb_lo = (int)(u / p.num_tiles) * p.kb_per_split;
+        const int nkb = (kb_lo + p.kb_per_split < p.k_blocks ? kb_lo + p.kb_per_split : p.k_blocks) - kb_lo;
         const int acc = it % C::ACC_BUFS;
         const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
         int kb = 0;
         if constexpr (SPLIT_RELEASE) {
-          const int early = p.k_blocks < STAGES ? p.k_blocks : STAGES;
+          const int early = nkb < STAGES ? nkb : STAGES;
           const int stage0 = stage;
           const uint32_t phase0 = phase;
           mbar_wait(&tmem_empty[0], acc_phase ^ 1);
@@ -345,7 +352,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
           tc_fence_after();
         }
-        for (; kb < p.k_blocks; ++kb) {
+        for (; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
@@ -373,9 +380,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     const int g = ew / 4;
     uint8_t *ebuf = smem_epi + ew * 2 * C::EPI_BUF_BYTES;
     int it = 0, chunk = 0;
-    for (int64_t t = cluster_id; t < p.num_tiles; t += num_clusters, ++it) {
+    for (int64_t u = cluster_id; u < p.num_units; u += num_clusters, ++it) {
+      const int64_t t = u % p.num_tiles;
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
+      b += (u / p.num_tiles) * p.batch;  // split-K slices are extra output batches
       const int acc = it % C::ACC_BUFS;
       const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
@@ -588,12 +597,14 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   memset(&mo, 0, sizeof(mo));
   const int oes = (int)sizeof(OutT);
   p.tma_store = ((uintptr_t)d.out % 16 == 0) && (d.o_stride[1] * oes) % 16 == 0 &&
-                (d.batch <= 1 || (d.o_stride[0] * oes) % 16 == 0) && !(p.debug & 2);
+                (d.batch * (p.k_splits > 1 ? p.k_splits : 1) <= 1 ||
+                 (d.o_stride[0] * oes) % 16 == 0) && !(p.debug & 2);
   if (p.tma_store) {
     const CUtensorMapDataType odt = oes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : (d.out_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
-    rc = make_map(&mo, d.out, odt, d.N, d.M, d.batch, d.o_stride[1], d.o_stride[0], 32, 32, oes,
+    rc = make_map(&mo, d.out, odt, d.N, d.M, d.batch * p.k_splits, d.o_stride[1], d.o_stride[0],
+                  32, 32, oes,
                   oes == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
@@ -602,6 +613,10 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   p.tiles_m = (int32_t)((d.M + C::TILE_M - 1) / C::TILE_M);
   p.tiles_n = (int32_t)((d.N + BN - 1) / BN);
   p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * d.batch;
+  if (p.k_splits < 1) p.k_splits = 1;
+  p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
+  p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
+  p.num_units = p.num_tiles * p.k_splits;
   auto kern = tc_gemm_kernel<BN, CG, OutT>;
   static thread_local int configured[64] = {0};
   static thread_local int clusters[64] = {0};
@@ -615,7 +630,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
     if (clusters[dev & 63] <= 0) clusters[dev & 63] = sm_count_current() / CG;
   }
   int64_t nclusters = clusters[dev & 63];
-  if (p.num_tiles < nclusters) nclusters = p.num_tiles;
+  if (p.num_units < nclusters) nclusters = p.num_units;
   if (d.sched.max_ctas > 0 && nclusters * CG > d.sched.max_ctas) nclusters = d.sched.max_ctas / CG;
   if (nclusters < 1) nclusters = 1;
   cudaLaunchConfig_t cfg{};
@@ -701,17 +716,21 @@ bool tc_legal(const bgx_contract_desc &d, const char **why) {
 
 void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out);
 
-int contract_tc(const bgx_contract_desc &d, cudaStream_t s) {
+namespace {
+int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s) {
   const char *why = nullptr;
   if (!tc_legal(d, &why)) {
     set_error("tensor-core path not legal: %s", why);
     return BGX_ERR_UNSUPPORTED;
   }
   TcParams p{};
+  p.k_splits = splits;
   p.batch = d.batch; p.M = d.M; p.N = d.N; p.K = d.K;
   p.a_mn = d.a_stride[2] != 1 ? 1 : 0;
   p.b_mn = d.b_stride[2] == 1 ? 1 : 0;
   p.k_blocks = (int32_t)((d.K + BK - 1) / BK);
+  if (p.k_splits > p.k_blocks) p.k_splits = p.k_blocks;
+  if (p.k_splits < 1) p.k_splits = 1;
   p.c0 = d.c0; p.out = d.out;
   for (int i = 0; i < 3; ++i) { p.sc[i] = d.c_stride[i]; p.so[i] = d.o_stride[i]; }
   int cg = 0, bn = 0;
@@ -726,6 +745,89 @@ int contract_tc(const bgx_contract_desc &d, cudaStream_t s) {
     return cg == 2 ? dispatch_bn<2, __nv_bfloat16>(d, bn, p, s)
                    : dispatch_bn<1, __nv_bfloat16>(d, bn, p, s);
   return cg == 2 ? dispatch_bn<2, __half>(d, bn, p, s) : dispatch_bn<1, __half>(d, bn, p, s);
+}
+
+// out[b,m,n] = (c0) + sum_s ws[s][b][m][n], summed in increasing s (deterministic).
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(const float *__restrict__ ws, int splits, int64_t batch, int64_t M,
+                     int64_t N, const OutT *__restrict__ c0, int64_t sc0, int64_t sc1,
+                     int64_t sc2, OutT *__restrict__ out, int64_t so0, int64_t so1, int64_t so2) {
+  const int64_t total = batch * M * N, slice = total;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i % N, m = (i / N) % M, b = i / (M * N);
+    float v = 0.f;
+    for (int sp = 0; sp < splits; ++sp) v = __fadd_rn(v, ws[sp * slice + i]);
+    if (c0) v = __fadd_rn(v, Conv<OutT>::to_f(c0[b * sc0 + m * sc1 + n * sc2]));
+    out[b * so0 + m * so1 + n * so2] = Conv<OutT>::from_f(v);
+  }
+}
+}  // namespace
+
+int contract_tc(const bgx_contract_desc &d, cudaStream_t s) { return contract_tc_impl(d, 1, s); }
+
+// Split-K plan: only when the (batch x M x N) tiles leave most SMs idle and K
+// is long enough to give every slice >= 8 k-blocks.
+void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) {
+  *splits = 1;
+  *ws_bytes = 0;
+  if (!tc_legal(d, nullptr)) return;
+  int cg = 0, bn = 0;
+  tc_tile_choice(d, &cg, &bn);
+  const int64_t tiles = ((d.M + 128 * cg - 1) / (128 * cg)) * ((d.N + bn - 1) / bn) * d.batch;
+  const int64_t slots = sm_count_current() / cg;
+  const int64_t k_blocks = (d.K + BK - 1) / BK;
+  if (tiles * 2 > slots || k_blocks < 16) return;
+  int64_t sp = slots / tiles;
+  if (sp > k_blocks / 8) sp = k_blocks / 8;
+  if (sp > 32) sp = 32;
+  if (sp < 2) return;
+  *splits = (int)sp;
+  *ws_bytes = sp * d.batch * d.M * d.N * 4;
+}
+
+int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t ws_bytes,
+                       cudaStream_t s) {
+  if (splits <= 1) return contract_tc(d, s);
+  BGX_CHECK_ARG(ws != nullptr && ((uintptr_t)ws % 16) == 0, "split-K: workspace must be 16B aligned");
+  BGX_CHECK_ARG(ws_bytes >= (int64_t)splits * d.batch * d.M * d.N * 4,
+                "split-K: workspace too small (%lld bytes for %d splits)", (long long)ws_bytes, splits);
+  bgx_contract_desc dp = d;
+  dp.out = ws;
+  dp.out_dtype = BGX_F32;
+  dp.c0 = nullptr;
+  dp.o_stride[0] = d.M * d.N;
+  dp.o_stride[1] = d.N;
+  dp.o_stride[2] = 1;
+  const int64_t k_blocks = (d.K + BK - 1) / BK;
+  const int64_t per = (k_blocks + splits - 1) / splits;
+  splits = (int)((k_blocks + per - 1) / per);   // the kernel normalises the same way
+  int rc = contract_tc_impl(dp, splits, s);
+  if (rc) return rc;
+  const int64_t total = d.batch * d.M * d.N;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = (int64_t)sm_count_current() * 16;
+  if (blocks > cap) blocks = cap;
+  switch (d.out_dtype) {
+    case BGX_F32:
+      splitk_reduce_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
+          (const float *)ws, splits, d.batch, d.M, d.N, (const float *)d.c0, d.c_stride[0],
+          d.c_stride[1], d.c_stride[2], (float *)d.out, d.o_stride[0], d.o_stride[1], d.o_stride[2]);
+      break;
+    case BGX_BF16:
+      splitk_reduce_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, s>>>(
+          (const float *)ws, splits, d.batch, d.M, d.N, (const __nv_bfloat16 *)d.c0,
+          d.c_stride[0], d.c_stride[1], d.c_stride[2], (__nv_bfloat16 *)d.out, d.o_stride[0],
+          d.o_stride[1], d.o_stride[2]);
+      break;
+    default:
+      splitk_reduce_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(
+          (const float *)ws, splits, d.batch, d.M, d.N, (const __half *)d.c0, d.c_stride[0],
+          d.c_stride[1], d.c_stride[2], (__half *)d.out, d.o_stride[0], d.o_stride[1],
+          d.o_stride[2]);
+  }
+  return check_launch("splitk_reduce_kernel");
 }
 
 // Tile shape the TC path would use (bgx_contract_tile).

@@ -137,6 +137,8 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
     d.mode = MODES[mode]
     if schedule:
         for k, v in schedule.items():
+            if k in ("splits", "no_splitk"):
+                continue
             if k == "reserved":
                 for i, x in enumerate(v):
                     d.sched.reserved[i] = int(x)
@@ -144,7 +146,20 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
                 setattr(d.sched, k, int(v))
     kind = lib.bgx_contract_kernel(d)
     _lib.check(kind if kind < 0 else 0, "bgx_contract_kernel")
+    splits = _lib._i32(1)
+    ws_bytes = _lib._i64(0)
+    if kind == _lib.KERNEL_TC and not (schedule and schedule.get("no_splitk")):
+        _lib.check(lib.bgx_contract_splitk_plan(d, splits, ws_bytes), "bgx_contract_splitk_plan")
+        if schedule and schedule.get("splits"):
+            splits.value = int(schedule["splits"])
+            ws_bytes.value = splits.value * batch * M * N * 4
     with torch.cuda.device(out.device):
+        if splits.value > 1:
+            ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=out.device)
+            _lib.check(lib.bgx_contract_splitk(d, splits.value, ws.data_ptr(), ws_bytes.value,
+                                               _stream_ptr(out)), "bgx_contract_splitk")
+            _log("tcgen05-splitk")
+            return kind
         _lib.check(lib.bgx_contract(d, _stream_ptr(out)), "bgx_contract")
     _log(_lib.KERNEL_NAMES.get(kind, "contract"))
     return kind

@@ -1,0 +1,70 @@
+"""Edge cases the reference handles: empty and extent-1 axes,
+empty reductions (K = 0 -> out = c0), rank-0 outputs, maximum operand count
+/ axis count of the generic kernel, non-contiguous views, and errors."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2503_04771_b200 import contract
+from paper_2503_04771_b200 import einsum as E
+from paper_2503_04771_b200 import interp as I
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ref_api(text, ins, init):
+    mod = E.build_einsum_function(None, E.parse_einsum(text))
+    vals = [I.TensorValue(E.F32, x.shape, x) for x in (*ins, init)]
+    [got] = I.run_function(mod, "einsum", vals, step_limit=None)
+    return got.data
+
+
+def oracle_of(text, ins, init):
+    s = E.parse_einsum(text)
+    return oracle.generic(s.inputs, s.output, ins, init)
+
+
+@pytest.mark.parametrize("text,shapes", [
+    ("(i,k),(k,j)->(i,j)", [(4, 0), (0, 5), (4, 5)]),      # empty reduction: out = c0
+    ("(i,k),(k,j)->(i,j)", [(0, 3), (3, 5), (0, 5)]),      # empty output
+    ("(i,j)->(i)", [(6, 0), (6,)]),
+    ("(i,j)->()", [(0, 4), ()]),
+    ("(i,k),(k,j)->(i,j)", [(1, 1), (1, 1), (1, 1)]),
+    ("(a,b,c,d,e),(e,f)->(a,b,c,d,f)", [(2, 1, 3, 1, 4), (4, 5), (2, 1, 3, 1, 5)]),
+    ("(a,b),(b,c),(c,d),(d,e),(e,f),(f,g)->(a,g)",
+     [(2, 3), (3, 2), (2, 3), (3, 2), (2, 2), (2, 3), (2, 3)]),  # 6 inputs (ABI max)
+    ("(i)->()", [(1000,), ()]),
+])
+def test_edge_shapes_bit_exact(dev, text, shapes):
+    rng = np.random.default_rng(0)
+    arrs = [rng.standard_normal(s).astype(np.float32) for s in shapes]
+    ins, init = arrs[:-1], arrs[-1]
+    got = run_ref_api(text, ins, init)
+    want = oracle_of(text, ins, init)
+    assert got.shape == want.shape
+    assert np.array_equal(got.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
+
+
+def test_bf16_empty_reduction_and_views(dev):
+    a = torch.randn(64, 0, device=dev).bfloat16()
+    b = torch.randn(0, 32, device=dev).bfloat16()
+    c0 = torch.randn(64, 32, device=dev).bfloat16()
+    out = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0)
+    assert torch.equal(out, c0)
+    big = torch.randn(300, 500, device=dev).bfloat16()
+    view = big[10:266:2, 100:420]          # strided rows (not TMA-legal -> copy / SIMT)
+    w = torch.randn(320, 96, device=dev).bfloat16()
+    got = contract("(i,k),(k,j)->(i,j)", view, w, out_dtype=torch.float32)
+    want = oracle.gemm_kseq(view.float().cpu().numpy(), w.float().cpu().numpy())
+    assert oracle.rel_frobenius(got.cpu().numpy(), want) <= 1e-2
+
+
+def test_errors_raise_without_fallback(dev):
+    with pytest.raises(ValueError, match="inconsistent extent"):
+        contract("(i,k),(k,j)->(i,j)", torch.zeros(4, 3, device=dev), torch.zeros(2, 5, device=dev))
+    with pytest.raises(ValueError, match="CUDA tensors only"):
+        contract("(i,k),(k,j)->(i,j)", torch.zeros(4, 3), torch.zeros(3, 5))
+    with pytest.raises(E.EinsumError):
+        contract("ij,jk->ik", torch.zeros(4, 3, device=dev), torch.zeros(3, 5, device=dev))

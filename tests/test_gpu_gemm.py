@@ -103,7 +103,7 @@ def test_tcgen05_layouts(dev, layout, dtype, M, N, K, cta_group, tile_n):
     executor.reset_launch_log()
     out = contract(spec, a, b, out_dtype=torch.float32, mode="tc",
                    schedule={"cta_group": cta_group, "tile_n": tile_n})
-    assert executor.launch_log() == ["tcgen05"]
+    assert [k.split("-")[0] for k in executor.launch_log()] == ["tcgen05"]
     A = np32(a) if spec.inputs[0] == ("i", "k") else np32(a).T
     B = np32(b) if spec.inputs[1] == ("k", "j") else np32(b).T
     want = oracle.gemm_kseq(np.ascontiguousarray(A), np.ascontiguousarray(B))
@@ -130,7 +130,7 @@ def test_tcgen05_batched_c3_pattern(dev):
     a, b = rnd((5, 192, 160), 31, dev, torch.bfloat16), rnd((5, 160, 272), 32, dev, torch.bfloat16)
     executor.reset_launch_log()
     out = contract("(b,i,j),(b,j,k)->(b,i,k)", a, b, out_dtype=torch.float32)
-    assert executor.launch_log() == ["tcgen05"]
+    assert [k.split("-")[0] for k in executor.launch_log()] == ["tcgen05"]
     want = oracle.gemm_kseq(np32(a), np32(b))
     assert oracle.rel_frobenius(np32(out), want) <= 1e-5
 
@@ -209,6 +209,41 @@ def test_tcgen05_unaligned_output_uses_direct_stores(dev, out_dtype, cta_group):
     executor.reset_launch_log()
     out = contract("(i,k),(j,k)->(i,j)", a, b, out_dtype=out_dtype, mode="tc",
                    schedule={"cta_group": cta_group})
-    assert executor.launch_log() == ["tcgen05"]
+    assert [k.split("-")[0] for k in executor.launch_log()] == ["tcgen05"]
     want = oracle.gemm_kseq(np32(a), np.ascontiguousarray(np32(b).T))
     assert oracle.rel_frobenius(np32(out), want) <= BF16_TOL
+
+
+@pytest.mark.parametrize("M,N,K,batch", [(256, 256, 16384, 1), (200, 136, 9000, 1), (128, 256, 4096, 3)])
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_splitk_matches_oracle(dev, M, N, K, batch, out_dtype):
+    """Small-output / long-K contractions split K across SMs (f32 partials +
+    in-order reduction); forced split counts and the automatic plan."""
+    a = rnd((batch, M, K), 61, dev, torch.bfloat16)
+    b = rnd((batch, K, N), 62, dev, torch.bfloat16)
+    c0 = rnd((batch, M, N), 63, dev, out_dtype)
+    want = oracle.gemm_kseq(np32(a), np32(b), np32(c0))
+    for sched in (None, {"splits": 3}, {"splits": 7, "cta_group": 2}):
+        executor.reset_launch_log()
+        out = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, c0=c0, out_dtype=out_dtype, schedule=sched)
+        log = executor.launch_log()
+        if sched:
+            assert log == ["tcgen05-splitk"], log
+        err = oracle.rel_frobenius(np32(out), want)
+        assert err <= (1e-5 if out_dtype == torch.float32 else BF16_TOL), (sched, err)
+
+
+def test_splitk_plan_only_for_small_outputs(dev):
+    import ctypes
+    a = rnd((8, 8), 1, dev, torch.bfloat16)
+    d = _lib.BgxContractDesc()
+    d.a = d.b = d.out = a.data_ptr()
+    d.in_dtype = d.out_dtype = _lib.BF16
+    sp, ws = ctypes.c_int32(), ctypes.c_int64()
+    for (M, N, K, expect) in [(256, 256, 1 << 20, True), (8192, 8192, 8192, False)]:
+        d.batch, d.M, d.N, d.K = 1, M, N, K
+        d.a_stride[:] = [0, K, 1]
+        d.b_stride[:] = [0, N, 1]
+        d.o_stride[:] = [0, N, 1]
+        assert _lib.load().bgx_contract_splitk_plan(d, sp, ws) == 0
+        assert (sp.value > 1) == expect and (ws.value > 0) == expect
