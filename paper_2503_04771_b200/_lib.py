@@ -22,7 +22,7 @@ MAX_OPERANDS = 6
 # bgx_dtype
 F32, F64, BF16, F16 = 0, 1, 2, 3
 # bgx_mode
-MODE_AUTO, MODE_EXACT, MODE_FFMA, MODE_TC, MODE_SIMT = 0, 1, 2, 3, 4
+MODE_AUTO, MODE_EXACT, MODE_FFMA, MODE_TC, MODE_SIMT, MODE_TF32 = 0, 1, 2, 3, 4, 5
 # bgx_contract_kernel results
 KERNEL_TC, KERNEL_EXACT, KERNEL_FFMA, KERNEL_SIMT16 = 1, 2, 3, 4
 KERNEL_NAMES = {KERNEL_TC: "tcgen05", KERNEL_EXACT: "simt-exact",

@@ -238,6 +238,29 @@ __device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64
         ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// kind::tf32 (fp32 storage, tf32 multiply, f32 accumulate); K = 8 per MMA.
+template <int CG>
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+template <int CG, int IN_BYTES>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                     uint32_t idesc, uint32_t accumulate) {
+  if constexpr (IN_BYTES == 4) umma_tf32<CG>(tmem_d, adesc, bdesc, idesc, accumulate);
+  else umma_f16<CG>(tmem_d, adesc, bdesc, idesc, accumulate);
+}
+
 // Signal `bar` when all previously issued tcgen05.mma of this thread retire.
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -294,6 +317,20 @@ __host__ __device__ __forceinline__ uint32_t make_idesc_f16(bool bf16, bool a_mn
   d |= 1u << 4;
   d |= fmt << 7;
   d |= fmt << 10;
+  d |= (a_mn_major ? 1u : 0u) << 15;
+  d |= (b_mn_major ? 1u : 0u) << 16;
+  d |= ((N >> 3) & 0x3Fu) << 17;
+  d |= ((M >> 4) & 0x1Fu) << 24;
+  return d;
+}
+
+// kind::tf32 instruction descriptor: a/b format TF32 = 2, otherwise as f16.
+__host__ __device__ __forceinline__ uint32_t make_idesc_tf32(bool a_mn_major, bool b_mn_major,
+                                                             uint32_t M, uint32_t N) {
+  uint32_t d = 0;
+  d |= 1u << 4;
+  d |= 2u << 7;
+  d |= 2u << 10;
   d |= (a_mn_major ? 1u : 0u) << 15;
   d |= (b_mn_major ? 1u : 0u) << 16;
   d |= ((N >> 3) & 0x3Fu) << 17;

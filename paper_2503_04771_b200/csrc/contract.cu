@@ -39,6 +39,18 @@ int select_kind(const bgx_contract_desc &d) {
     }
     case BGX_MODE_SIMT:
       return half_in ? KIND_SIMT16 : KIND_EXACT;
+    case BGX_MODE_TF32: {
+      const char *why = nullptr;
+      if (d.in_dtype != BGX_F32) {
+        set_error("bgx_contract: TF32 mode needs f32 inputs");
+        return BGX_ERR_UNSUPPORTED;
+      }
+      if (!tc_legal(d, &why)) {
+        set_error("bgx_contract: tf32 tensor-core path not legal: %s", why);
+        return BGX_ERR_UNSUPPORTED;
+      }
+      return KIND_TC;
+    }
     default:
       set_error("bgx_contract: bad mode %d", d.mode);
       return BGX_ERR_INVALID;

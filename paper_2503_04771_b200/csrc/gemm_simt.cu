@@ -123,6 +123,103 @@ simt_gemm_kernel(const Params p) {
     }
 }
 
+// 128 x 128 tile, 256 threads, 8 x 8 outputs per thread (two 4-wide groups in
+// each dimension so shared-memory fragment reads are broadcast / 16-byte),
+// BK = 8, double-buffered shared memory with register prefetch of the next
+// k-tile.  Each output still accumulates its products in increasing k from
+// c0, so EXACT mode stays bit-identical to the reference.
+constexpr int BT = 128, BKB = 8;
+
+template <typename In, typename Out, typename Acc, bool FUSED>
+__global__ void __launch_bounds__(256)
+simt_gemm_big_kernel(const Params p) {
+  __shared__ __align__(16) Acc As[2][BKB][BT];
+  __shared__ __align__(16) Acc Bs[2][BKB][BT];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  int64_t t = blockIdx.x;
+  const int64_t tn = t % p.tiles_n;
+  t /= p.tiles_n;
+  const int64_t tm = t % p.tiles_m;
+  const int64_t b = t / p.tiles_m;
+  const int64_t m0 = tm * BT, n0 = tn * BT;
+  const In *A = static_cast<const In *>(p.a) + b * p.sa[0];
+  const In *B = static_cast<const In *>(p.b) + b * p.sb[0];
+  // load mappings: 4 elements per thread per operand per k-tile
+  const bool a_k = p.sa[2] == 1;
+  const bool b_n = p.sb[2] == 1 || p.sb[1] != 1;
+  const int a_r = a_k ? tid / 2 : (tid % 32) * 4, a_c = a_k ? (tid % 2) * 4 : tid / 32;
+  const int b_r = b_n ? tid / 32 : (tid % 2) * 4, b_c = b_n ? (tid % 32) * 4 : tid / 2;
+  Acc ra[4], rb[4];
+  auto load_tiles = [&](int64_t k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int mm = a_k ? a_r : a_r + q, kk = a_k ? a_c + q : a_c;
+      const int64_t m = m0 + mm, k = k0 + kk;
+      ra[q] = (m < p.M && k < p.K) ? to_acc<In, Acc>(A[m * p.sa[1] + k * p.sa[2]]) : (Acc)0;
+      const int kb_ = b_n ? b_r : b_r + q, nn = b_n ? b_c + q : b_c;
+      const int64_t kb2 = k0 + kb_, n = n0 + nn;
+      rb[q] = (n < p.N && kb2 < p.K) ? to_acc<In, Acc>(B[kb2 * p.sb[1] + n * p.sb[2]]) : (Acc)0;
+    }
+  };
+  auto store_tiles = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (a_k) As[buf][a_c + q][a_r] = ra[q]; else As[buf][a_c][a_r + q] = ra[q];
+      if (b_n) Bs[buf][b_r][b_c + q] = rb[q]; else Bs[buf][b_r + q][b_c] = rb[q];
+    }
+  };
+  Acc acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      Acc v = (Acc)0;
+      if (p.c0 && m < p.M && n < p.N)
+        v = to_acc<Out, Acc>(static_cast<const Out *>(p.c0)[b * p.sc[0] + m * p.sc[1] + n * p.sc[2]]);
+      acc[i][j] = v;
+    }
+  const int64_t ktiles = (p.K + BKB - 1) / BKB;
+  if (ktiles > 0) {
+    load_tiles(0);
+    store_tiles(0);
+  }
+  __syncthreads();
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) load_tiles((kt + 1) * BKB);   // in flight during the math
+    const int kmax = (p.K - kt * BKB) < BKB ? (int)(p.K - kt * BKB) : BKB;
+#pragma unroll
+    for (int kk = 0; kk < BKB; ++kk) {
+      if (kk >= kmax) break;
+      Acc av[8], bv[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        av[i] = As[buf][kk][ty * 4 + i];
+        av[4 + i] = As[buf][kk][64 + ty * 4 + i];
+        bv[i] = Bs[buf][kk][tx * 4 + i];
+        bv[4 + i] = Bs[buf][kk][64 + tx * 4 + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = Arith<Acc>::template mac<FUSED>(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < ktiles) store_tiles(buf ^ 1);
+    __syncthreads();
+  }
+  Out *O = static_cast<Out *>(p.out) + b * p.so[0];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (m < p.M && n < p.N) O[m * p.so[1] + n * p.so[2]] = from_acc<Out, Acc>(acc[i][j]);
+    }
+}
+
 template <typename In, typename Out, typename Acc, bool FUSED>
 int launch(const bgx_contract_desc &d, cudaStream_t s) {
   Params p;
@@ -138,11 +235,16 @@ int launch(const bgx_contract_desc &d, cudaStream_t s) {
     p.tiles_m = (d.M + 31) / 32; p.tiles_n = (d.N + 31) / 32;
     int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
     simt_gemm_kernel<In, Out, Acc, FUSED, 32, 32><<<(unsigned)blocks, 64, 0, s>>>(p);
-  } else {
+  } else if ((d.M * d.N * d.batch) < (int64_t)sms * BT * BT) {
     p.tiles_m = (d.M + 63) / 64; p.tiles_n = (d.N + 63) / 64;
     int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
     if (blocks > 0x7fffffffLL) { set_error("simt gemm: grid too large"); return BGX_ERR_UNSUPPORTED; }
     simt_gemm_kernel<In, Out, Acc, FUSED, 64, 64><<<(unsigned)blocks, 256, 0, s>>>(p);
+  } else {
+    p.tiles_m = (d.M + BT - 1) / BT; p.tiles_n = (d.N + BT - 1) / BT;
+    int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
+    if (blocks > 0x7fffffffLL) { set_error("simt gemm: grid too large"); return BGX_ERR_UNSUPPORTED; }
+    simt_gemm_big_kernel<In, Out, Acc, FUSED><<<(unsigned)blocks, 256, 0, s>>>(p);
   }
   return check_launch("simt_gemm_kernel");
 }

@@ -39,8 +39,15 @@ namespace bgx {
 namespace {
 
 constexpr int BM = 128;                     // rows of A per CTA
-constexpr int BK = 64;                      // 64 x 16-bit = 128 B = one swizzle row
-constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int ROW_BYTES = 128;              // one 128B-swizzle row of K per k-block
+constexpr int A_STAGE_BYTES = BM * ROW_BYTES;  // 16 KB
+// K elements per k-block: 64 for 16-bit inputs, 32 for tf32 (fp32 storage)
+template <int IN_BYTES> struct Elem {
+  static constexpr int BK = ROW_BYTES / IN_BYTES;
+  static constexpr int MMA_K = 32 / IN_BYTES;        // K per tcgen05.mma (16 / 8)
+  static constexpr int MN_ATOM = ROW_BYTES / IN_BYTES;  // MN elements per swizzle row
+  static constexpr int BOX_BYTES = MN_ATOM * BK * IN_BYTES;  // one MN-major box (8 / 4 KB)
+};
 constexpr int EPI_WARPS = 8;                // 2 warps per TMEM lane quadrant
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int SMEM_BUDGET = 227 * 1024;
@@ -60,15 +67,16 @@ struct TcParams {
   void *out; int64_t so[3];
 };
 
-template <int BN, int CG, int OUT_BYTES> struct Cfg {
+template <int BN, int CG, int OUT_BYTES, int IN_BYTES = 2> struct Cfg {
+  using E = Elem<IN_BYTES>;
   static constexpr int BN_CTA = BN / CG;                 // B columns staged per CTA
   // one tcgen05.mma covers at most N = 256: wider tiles issue NSPLIT MMAs per
   // K-step into adjacent TMEM column ranges
   static constexpr int MMA_N = BN > 256 ? 256 : BN;
   static constexpr int NSPLIT = BN / MMA_N;
   static constexpr int B_BOX_N = MMA_N / CG;             // B columns per CTA per MMA
-  static constexpr int B_HALF_BYTES = B_BOX_N * BK * 2;
-  static constexpr int B_STAGE_BYTES = BN_CTA * BK * 2;
+  static constexpr int B_HALF_BYTES = B_BOX_N * ROW_BYTES;
+  static constexpr int B_STAGE_BYTES = BN_CTA * ROW_BYTES;
   static constexpr int ACC_BUFS = 2 * BN <= 512 ? 2 : 1; // double-buffered accumulator?
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
   // epilogue staging: 4 warps x 2 buffers x (32 rows x 32 cols) of the output
@@ -179,12 +187,14 @@ __device__ __forceinline__ void tma_load(void *dst, const void *tmap, uint64_t *
   else tma_load_3d_cg2(dst, tmap, bar, c0, c1, c2);
 }
 
-template <int BN, int CG, typename OutT>
+template <int BN, int CG, typename OutT, int IN_BYTES>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                const __grid_constant__ CUtensorMap tmap_b,
                const __grid_constant__ CUtensorMap tmap_o, const TcParams p) {
-  using C = Cfg<BN, CG, (int)sizeof(OutT)>;
+  using C = Cfg<BN, CG, (int)sizeof(OutT), IN_BYTES>;
+  using E = typename C::E;
+  constexpr int BK = E::BK;
   constexpr int MAX_STAGES = C::STAGES;
   const int STAGES = p.stages;
   constexpr int BN_CTA = C::BN_CTA;
@@ -256,12 +266,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
           if (leader) mbar_expect_tx(&full[stage], CG * C::STAGE_BYTES);
-          const int32_t k0 = kb * BK;
+          const int32_t k0 = kb * BK;  // in elements
           uint8_t *sa = smem_a + stage * A_STAGE_BYTES;
           uint8_t *sb = smem_b + stage * C::B_STAGE_BYTES;
           if (p.a_mn) {
-            tma_load<CG>(sa, &tmap_a, &full[stage], m0, k0, bb);
-            tma_load<CG>(sa + 8192, &tmap_a, &full[stage], m0 + 64, k0, bb);
+#pragma unroll
+            for (int j = 0; j < BM / E::MN_ATOM; ++j)
+              tma_load<CG>(sa + j * E::BOX_BYTES, &tmap_a, &full[stage], m0 + E::MN_ATOM * j, k0, bb);
           } else {
             tma_load<CG>(sa, &tmap_a, &full[stage], k0, m0, bb);
           }
@@ -271,8 +282,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
             const int32_t nh = n0 + h * C::MMA_N;
             if (p.b_mn) {
 #pragma unroll
-              for (int j = 0; j < C::B_BOX_N / 64; ++j)
-                tma_load<CG>(sbh + j * 8192, &tmap_b, &full[stage], nh + 64 * j, k0, bb);
+              for (int j = 0; j < C::B_BOX_N / E::MN_ATOM; ++j)
+                tma_load<CG>(sbh + j * E::BOX_BYTES, &tmap_b, &full[stage], nh + E::MN_ATOM * j,
+                             k0, bb);
             } else {
               tma_load<CG>(sbh, &tmap_b, &full[stage], k0, nh, bb);
             }
@@ -290,9 +302,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       int it = 0;
       // Descriptor = {lo: start>>4 | LBO>>4 << 16, hi: SBO>>4 | version | SW128}:
       // only the start-address field moves along K, so precompute the rest.
-      const uint32_t a_step = (p.a_mn ? 2048u : 32u) >> 4, b_step = (p.b_mn ? 2048u : 32u) >> 4;
-      const uint64_t a_fixed = make_sdesc_sw128(0, p.a_mn ? 8192u : 16u, 1024);
-      const uint64_t b_fixed = make_sdesc_sw128(0, p.b_mn ? 8192u : 16u, 1024);
+      // per-MMA K advance: 32 bytes along a K-major row, or MMA_K rows of 128 B
+      // for MN-major; MN-major LBO = one box (MN_ATOM x BK), SBO = 8 rows
+      constexpr uint32_t MN_STEP = E::MMA_K * ROW_BYTES;
+      const uint32_t a_step = (p.a_mn ? MN_STEP : 32u) >> 4, b_step = (p.b_mn ? MN_STEP : 32u) >> 4;
+      const uint64_t a_fixed = make_sdesc_sw128(0, p.a_mn ? (uint32_t)E::BOX_BYTES : 16u, 1024);
+      const uint64_t b_fixed = make_sdesc_sw128(0, p.b_mn ? (uint32_t)E::BOX_BYTES : 16u, 1024);
       const uint32_t sa0 = smem_u32(smem_a) >> 4, sb0 = smem_u32(smem_b) >> 4;
       // With a single 512-column accumulator (BN = 512) the two N = 256 halves
       // are released separately by the epilogue (tmem_empty[0] = columns
@@ -303,13 +318,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         const uint64_t ad0 = a_fixed | (uint64_t)(sa0 + st * (A_STAGE_BYTES >> 4));
         const uint64_t bd0 = b_fixed | (uint64_t)(sb0 + st * (C::B_STAGE_BYTES >> 4));
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
+        for (int k = 0; k < BK / E::MMA_K; ++k)
 #pragma unroll
           for (int h = 0; h < C::NSPLIT; ++h)
             if (h >= h_lo && h < h_hi)
-              umma_f16<CG>(d_tmem + h * C::MMA_N, ad0 + k * a_step,
-                           bd0 + h * (C::B_HALF_BYTES >> 4) + k * b_step, p.idesc,
-                           (kb | k) != 0);
+              umma<CG, IN_BYTES>(d_tmem + h * C::MMA_N, ad0 + k * a_step,
+                                 bd0 + h * (C::B_HALF_BYTES >> 4) + k * b_step, p.idesc,
+                                 (kb | k) != 0);
       };
       auto release = [&](int st) {
         if constexpr (CG == 1) umma_commit(&empty[st]);
@@ -573,23 +588,27 @@ int max_clusters(K kern, int smem, int cg) {
   return n;
 }
 
-template <int BN, int CG, typename OutT>
+template <int BN, int CG, typename OutT, int IN_BYTES>
 int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
-  using C = Cfg<BN, CG, (int)sizeof(OutT)>;
+  using C = Cfg<BN, CG, (int)sizeof(OutT), IN_BYTES>;
+  using E = typename C::E;
   TcParams p = p0;
-  const CUtensorMapDataType dt =
-      d.in_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapDataType dt = IN_BYTES == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : d.in_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap ma, mb;
   int rc;
+  constexpr uint32_t AT = E::MN_ATOM, KB = E::BK;
   if (p.a_mn)
-    rc = make_map(&ma, d.a, dt, d.M, d.K, d.batch, d.a_stride[2], d.a_stride[0], 64, 64);
+    rc = make_map(&ma, d.a, dt, d.M, d.K, d.batch, d.a_stride[2], d.a_stride[0], AT, KB, IN_BYTES);
   else
-    rc = make_map(&ma, d.a, dt, d.K, d.M, d.batch, d.a_stride[1], d.a_stride[0], 64, BM);
+    rc = make_map(&ma, d.a, dt, d.K, d.M, d.batch, d.a_stride[1], d.a_stride[0], KB, BM, IN_BYTES);
   if (rc) return rc;
   if (p.b_mn)
-    rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], 64, 64);
+    rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], AT, KB, IN_BYTES);
   else
-    rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], 64, C::B_BOX_N);
+    rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], KB, C::B_BOX_N,
+                  IN_BYTES);
   if (rc) return rc;
   // output map for the TMA-store epilogue (falls back to direct stores when
   // the output's row/batch strides are not 16-byte multiples)
@@ -608,7 +627,8 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
                   oes == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
-  p.idesc = make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, C::MMA_N);
+  p.idesc = IN_BYTES == 4 ? make_idesc_tf32(p.a_mn, p.b_mn, C::TILE_M, C::MMA_N)
+                          : make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, C::MMA_N);
   p.stages = (d.sched.stages >= 2 && d.sched.stages <= C::STAGES) ? d.sched.stages : C::STAGES;
   p.tiles_m = (int32_t)((d.M + C::TILE_M - 1) / C::TILE_M);
   p.tiles_n = (int32_t)((d.N + BN - 1) / BN);
@@ -617,7 +637,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   p.num_units = p.num_tiles * p.k_splits;
-  auto kern = tc_gemm_kernel<BN, CG, OutT>;
+  auto kern = tc_gemm_kernel<BN, CG, OutT, IN_BYTES>;
   static thread_local int configured[64] = {0};
   static thread_local int clusters[64] = {0};
   int dev = 0;
@@ -649,13 +669,15 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   return check_launch("tc_gemm_kernel");
 }
 
-template <int CG, typename OutT>
+template <int CG, typename OutT, int IB = 2>
 int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStream_t s) {
   switch (bn) {
-    case 64: return CG == 1 ? launch_tc<64, 1, OutT>(d, p, s) : launch_tc<128, CG, OutT>(d, p, s);
-    case 128: return launch_tc<128, CG, OutT>(d, p, s);
-    case 512: return CG == 2 ? launch_tc<512, 2, OutT>(d, p, s) : launch_tc<256, CG, OutT>(d, p, s);
-    default: return launch_tc<256, CG, OutT>(d, p, s);
+    case 64:
+      return CG == 1 ? launch_tc<64, 1, OutT, IB>(d, p, s) : launch_tc<128, CG, OutT, IB>(d, p, s);
+    case 128: return launch_tc<128, CG, OutT, IB>(d, p, s);
+    case 512:
+      return CG == 2 ? launch_tc<512, 2, OutT, IB>(d, p, s) : launch_tc<256, CG, OutT, IB>(d, p, s);
+    default: return launch_tc<256, CG, OutT, IB>(d, p, s);
   }
 }
 
@@ -693,8 +715,15 @@ void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
 // Legality of the TMA/tcgen05 path for a descriptor (see bgx.h).
 bool tc_legal(const bgx_contract_desc &d, const char **why) {
   auto fail = [&](const char *w) { if (why) *why = w; return false; };
-  if (!(d.in_dtype == BGX_BF16 || d.in_dtype == BGX_F16)) return fail("inputs not bf16/f16");
+  const bool tf32 = d.in_dtype == BGX_F32 && d.mode == BGX_MODE_TF32;
+  if (!(d.in_dtype == BGX_BF16 || d.in_dtype == BGX_F16 || tf32))
+    return fail("inputs not bf16/f16 (or f32 with BGX_MODE_TF32)");
   if (!(d.out_dtype == d.in_dtype || d.out_dtype == BGX_F32)) return fail("out dtype");
+  const int es = tf32 ? 4 : 2;
+  // MN-major 32-bit operands need the SWIZZLE_128B_BASE32B UMMA layout (not
+  // implemented): tf32 takes K-major A and B; callers transpose otherwise.
+  if (tf32 && (d.a_stride[2] != 1 || (d.b_stride[1] != 1 && !(d.K == 1))))
+    return fail("tf32 needs K-major A and B (k unit stride)");
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0) return fail("empty extent");
   if (d.M >= (1ll << 31) || d.N >= (1ll << 31) || d.K >= (1ll << 31)) return fail("extent >= 2^31");
   const bool a_mn = d.a_stride[2] != 1 && d.a_stride[1] == 1;
@@ -703,7 +732,7 @@ bool tc_legal(const bgx_contract_desc &d, const char **why) {
   const bool b_mn = d.b_stride[2] == 1;
   const bool b_k = !b_mn && d.b_stride[1] == 1;
   if (!b_mn && !b_k) return fail("B has no unit stride in k or n");
-  auto al16 = [](int64_t elems) { return (elems * 2) % 16 == 0; };
+  auto al16 = [es](int64_t elems) { return (elems * es) % 16 == 0; };
   if (((uintptr_t)d.a % 16) || ((uintptr_t)d.b % 16)) return fail("A/B base not 16B aligned");
   if (a_k && (!al16(d.a_stride[1]) || (d.batch > 1 && !al16(d.a_stride[0])))) return fail("A strides");
   if (a_mn && (!al16(d.a_stride[2]) || (d.batch > 1 && !al16(d.a_stride[0])))) return fail("A strides");
@@ -728,7 +757,8 @@ int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s) {
   p.batch = d.batch; p.M = d.M; p.N = d.N; p.K = d.K;
   p.a_mn = d.a_stride[2] != 1 ? 1 : 0;
   p.b_mn = d.b_stride[2] == 1 ? 1 : 0;
-  p.k_blocks = (int32_t)((d.K + BK - 1) / BK);
+  const int BKe = d.in_dtype == BGX_F32 ? Elem<4>::BK : Elem<2>::BK;
+  p.k_blocks = (int32_t)((d.K + BKe - 1) / BKe);
   if (p.k_splits > p.k_blocks) p.k_splits = p.k_blocks;
   if (p.k_splits < 1) p.k_splits = 1;
   p.c0 = d.c0; p.out = d.out;
@@ -739,6 +769,8 @@ int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s) {
   // columns) L2-resident while A streams (-8); otherwise M-groups.
   p.raster = d.sched.raster != 0 ? d.sched.raster : (bn == 512 ? -8 : (cg == 2 ? 8 : 16));
   p.debug = d.sched.reserved[0];
+  if (d.in_dtype == BGX_F32)  // tf32 tensor cores (opt-in BGX_MODE_TF32)
+    return cg == 2 ? dispatch_bn<2, float, 4>(d, bn, p, s) : dispatch_bn<1, float, 4>(d, bn, p, s);
   if (d.out_dtype == BGX_F32)
     return cg == 2 ? dispatch_bn<2, float>(d, bn, p, s) : dispatch_bn<1, float>(d, bn, p, s);
   if (d.out_dtype == BGX_BF16)
@@ -777,7 +809,8 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
   tc_tile_choice(d, &cg, &bn);
   const int64_t tiles = ((d.M + 128 * cg - 1) / (128 * cg)) * ((d.N + bn - 1) / bn) * d.batch;
   const int64_t slots = sm_count_current() / cg;
-  const int64_t k_blocks = (d.K + BK - 1) / BK;
+  const int BKe = d.in_dtype == BGX_F32 ? Elem<4>::BK : Elem<2>::BK;
+  const int64_t k_blocks = (d.K + BKe - 1) / BKe;
   if (tiles * 2 > slots || k_blocks < 16) return;
   int64_t sp = slots / tiles;
   if (sp > k_blocks / 8) sp = k_blocks / 8;
@@ -800,7 +833,8 @@ int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t
   dp.o_stride[0] = d.M * d.N;
   dp.o_stride[1] = d.N;
   dp.o_stride[2] = 1;
-  const int64_t k_blocks = (d.K + BK - 1) / BK;
+  const int BKe = d.in_dtype == BGX_F32 ? Elem<4>::BK : Elem<2>::BK;
+  const int64_t k_blocks = (d.K + BKe - 1) / BKe;
   const int64_t per = (k_blocks + splits - 1) / splits;
   splits = (int)((k_blocks + per - 1) / per);   // the kernel normalises the same way
   int rc = contract_tc_impl(dp, splits, s);

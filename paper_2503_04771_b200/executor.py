@@ -26,7 +26,7 @@ TORCH_TO_BGX = {torch.float32: _lib.F32, torch.float64: _lib.F64,
 DTYPE_NAME = {torch.float32: "f32", torch.float64: "f64", torch.bfloat16: "bf16",
               torch.float16: "f16"}
 MODES = {"auto": _lib.MODE_AUTO, "exact": _lib.MODE_EXACT, "ffma": _lib.MODE_FFMA,
-         "tc": _lib.MODE_TC, "simt": _lib.MODE_SIMT}
+         "tc": _lib.MODE_TC, "simt": _lib.MODE_SIMT, "tf32": _lib.MODE_TF32}
 
 _trace = threading.local()
 
@@ -123,6 +123,16 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
     """One ``bgx_contract`` call on raw (tensor, 3 strides) views; returns the
     kernel id that ran (_lib.KERNEL_*)."""
     lib = _lib.load()
+    if mode == "tf32":
+        # the tf32 kernel takes K-major operands: materialise others once
+        if a_strides[2] != 1 and K > 1:
+            a3 = torch.as_strided(a, (batch, M, K), a_strides)
+            a = permute(a3, torch.empty((batch, M, K), dtype=a.dtype, device=a.device), (0, 1, 2))
+            a_strides = (M * K, K, 1)
+        if b_strides[1] != 1 and K > 1:
+            b3 = torch.as_strided(b, (batch, K, N), b_strides)
+            b = permute(b3, torch.empty((batch, N, K), dtype=b.dtype, device=b.device), (0, 2, 1))
+            b_strides = (N * K, 1, K)
     d = _lib.BgxContractDesc()
     d.batch, d.M, d.N, d.K = batch, M, N, K
     d.a = a.data_ptr() if a is not None else None

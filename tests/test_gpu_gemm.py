@@ -247,3 +247,38 @@ def test_splitk_plan_only_for_small_outputs(dev):
         d.o_stride[:] = [0, N, 1]
         assert _lib.load().bgx_contract_splitk_plan(d, sp, ws) == 0
         assert (sp.value > 1) == expect and (ws.value > 0) == expect
+
+
+TF32_TOL = 5e-3   # 10-bit mantissa products, f32 accumulation
+
+
+@pytest.mark.parametrize("layout", list(LAYOUTS))
+@pytest.mark.parametrize("cta_group,tile_n", [(1, 0), (2, 0), (2, 512)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 96), (1000, 520, 1000)])
+def test_tf32_tensor_cores(dev, layout, cta_group, tile_n, M, N, K):
+    """f32 inputs on tcgen05 kind::tf32 (opt-in mode='tf32')."""
+    spec = E.parse_einsum(LAYOUTS[layout])
+    shp = {"i": M, "j": N, "k": K}
+    a = rnd(tuple(shp[x] for x in spec.inputs[0]), 71, dev)
+    b = rnd(tuple(shp[x] for x in spec.inputs[1]), 72, dev)
+    executor.reset_launch_log()
+    out = contract(spec, a, b, mode="tf32", schedule={"cta_group": cta_group, "tile_n": tile_n})
+    # MN-major operands are first made K-major by bgx_permute (tf32 kernel limit)
+    assert [k.split("-")[0] for k in executor.launch_log() if k != "permute"] == ["tcgen05"]
+    A = np32(a) if spec.inputs[0] == ("i", "k") else np32(a).T
+    B = np32(b) if spec.inputs[1] == ("k", "j") else np32(b).T
+    want = oracle.gemm_kseq(np.ascontiguousarray(A), np.ascontiguousarray(B))
+    err = oracle.rel_frobenius(np32(out), want)
+    assert 1e-7 < err <= TF32_TOL, err   # tf32 really is lower precision than f32 FFMA
+
+
+def test_tf32_c1_config_and_splitk(dev):
+    a, b = rnd((256, 256), 1, dev), rnd((256, 256), 2, dev)
+    out = contract("(i,j),(j,k)->(i,k)", a, b, mode="tf32")
+    assert oracle.rel_frobenius(np32(out), oracle.gemm_kseq(np32(a), np32(b))) <= TF32_TOL
+    a, b = rnd((128, 65536), 3, dev), rnd((65536, 128), 4, dev)
+    executor.reset_launch_log()
+    out = contract("(i,k),(k,j)->(i,j)", a, b, mode="tf32")
+    assert [k for k in executor.launch_log() if k != "permute"] == ["tcgen05-splitk"]
+    ref = oracle.gemm_kseq(np32(a), np32(b))
+    assert oracle.rel_frobenius(np32(out), ref) <= TF32_TOL
