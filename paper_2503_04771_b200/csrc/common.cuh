@@ -76,6 +76,19 @@ template <> struct Conv<__half> {
   __device__ static __half from_f(float v) { return __float2half_rn(v); }
 };
 
+// Two f32 -> packed 16-bit pair (lo in bits 0-15), round-to-nearest-even.
+template <typename H> __device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <> __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // PTX wrappers (sm_100a)
 

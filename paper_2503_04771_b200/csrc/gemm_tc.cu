@@ -135,11 +135,7 @@ __device__ __forceinline__ void stage_row32(uint8_t *buf, int r, const float *v)
       uint4 pk;
       uint32_t *w = reinterpret_cast<uint32_t *>(&pk);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        OutT lo = Conv<OutT>::from_f(v[8 * j + 2 * q]), hi = Conv<OutT>::from_f(v[8 * j + 2 * q + 1]);
-        w[q] = (uint32_t)(*reinterpret_cast<uint16_t *>(&lo)) |
-               ((uint32_t)(*reinterpret_cast<uint16_t *>(&hi)) << 16);
-      }
+      for (int q = 0; q < 4; ++q) w[q] = pack2<OutT>(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
       *reinterpret_cast<uint4 *>(buf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) = pk;
     }
   }
@@ -442,12 +438,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
               tmem_ld_32x32b_x32(taddr + c * 32, r);
               tmem_ld_wait();
 #pragma unroll
-              for (int q = 0; q < 16; ++q) {
-                OutT lo = Conv<OutT>::from_f(__uint_as_float(r[2 * q]));
-                OutT hi = Conv<OutT>::from_f(__uint_as_float(r[2 * q + 1]));
-                pk[j][q] = (uint32_t)(*reinterpret_cast<uint16_t *>(&lo)) |
-                           ((uint32_t)(*reinterpret_cast<uint16_t *>(&hi)) << 16);
-              }
+              for (int q = 0; q < 16; ++q)
+                pk[j][q] = pack2<OutT>(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
             }
             arrive_empty(half);   // this half of TMEM is free for the next tile
 #pragma unroll

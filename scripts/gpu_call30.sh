@@ -1,0 +1,25 @@
+#!/bin/bash
+P2="python scripts/profile_kernels.py --what chain_gemm --reps 1 --cg 2 --tile-n 512 --rasters -8 --debugs 0,16,4"
+$P2 > gpurun_out/plain30.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --clock-control none -k regex:tc_gemm --csv --log-file gpurun_out/ours30.csv $P2 > gpurun_out/ncu30.log 2>&1; echo "ncu rc=$?"; grep -v "^==" gpurun_out/ours30.csv | cut -d, -f12- | tail -6
+python - <<'PY' > gpurun_out/power30.txt 2>&1
+import sys
+sys.path.insert(0, 'scripts')
+src = open('scripts/power_compare.py').read().split('\nfor rep in range(')[0]
+exec(src)
+def ours_bn(bn, raster=0, cg=2, dbg=0):
+    d = _lib.BgxContractDesc()
+    d.batch, d.M, d.N, d.K = 1, M, N, K
+    d.a, d.b, d.out = a.data_ptr(), b.data_ptr(), out.data_ptr()
+    d.a_stride[:] = [0, K, 1]; d.b_stride[:] = [0, N, 1]; d.o_stride[:] = [0, N, 1]
+    d.in_dtype = d.out_dtype = _lib.BF16; d.mode = _lib.MODE_TC
+    d.sched.cta_group, d.sched.tile_n, d.sched.raster = cg, bn, raster
+    d.sched.reserved[0] = dbg
+    sp = torch.cuda.current_stream().cuda_stream
+    return lambda: lib.bgx_contract(d, sp)
+for rep in range(2):
+    run("cuBLAS", lambda: torch.matmul(a, b, out=out))
+    run("ours 2x512 tma-store", ours_bn(512, -8))
+    run("ours 2x512 direct", ours_bn(512, -8, dbg=16))
+PY
+cat gpurun_out/power30.txt
