@@ -130,7 +130,8 @@ def barrier_sync(world):
 def max_over_ranks(x: float, world: int) -> float:
     if world == 1:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -353,10 +354,18 @@ def main():
         return run_reference(args)
 
     world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; BGX_DIST_BACKEND=gloo (functional testing of the
+    # multi-rank path on fewer GPUs — the data path has no collective, only
+    # the barrier / max-over-ranks timing uses the process group)
+    backend = os.environ.get("BGX_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2503_04771_b200 import _lib, executor, shard
     from paper_2503_04771_b200.api import contract_host
     _lib.load()
@@ -390,7 +399,7 @@ def main():
     barrier_sync(world)
     executor.reset_launch_log()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         t0.record(stream)
         for _ in range(args.steps):
             step(record=True)
