@@ -47,13 +47,52 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
       continue;
     }
     T acc = static_cast<const T *>(d.c0)[o];
-    int64_t idx[BGX_MAX_AXES];
-    for (int a = 0; a < n_red; ++a) idx[a] = 0;
-    for (int64_t r = 0; r < red_points; ++r) {
+    if (red_points == 0) {
+      static_cast<T *>(d.out)[o] = acc;
+      continue;
+    }
+    if (n_red == 0) {  // elementwise body (Hadamard / outer product): one point
       T p = ins[0][off[0]];
       for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k]]);
-      acc = add_rn<T>(p, acc);
-      for (int a = n_red - 1; a >= 0; --a) {
+      static_cast<T *>(d.out)[o] = add_rn<T>(p, acc);
+      continue;
+    }
+    // Innermost reduction axis: U points of every operand are loaded ahead
+    // (independent loads in flight), then folded into the running sum in the
+    // reference's order — same arithmetic sequence, latency hidden.
+    constexpr int U = 8;
+    const int ax_in = n_axes - 1;
+    const int64_t E = d.extents[ax_in];
+    int64_t sin[BGX_MAX_OPERANDS];
+    for (int k = 0; k < n_in; ++k) sin[k] = d.strides[k][ax_in];
+    const int64_t outer = red_points / E;
+    int64_t idx[BGX_MAX_AXES];
+    for (int a = 0; a < n_red - 1; ++a) idx[a] = 0;
+    for (int64_t r = 0; r < outer; ++r) {
+      int64_t j = 0;
+      for (; j + U <= E; j += U) {
+        T v[NIN > 0 ? NIN : BGX_MAX_OPERANDS][U];
+#pragma unroll
+        for (int k = 0; k < (NIN > 0 ? NIN : BGX_MAX_OPERANDS); ++k) {
+          if (k >= n_in) break;
+          const T *base = ins[k] + off[k] + j * sin[k];
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[k][u] = base[u * sin[k]];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          T p = v[0][u];
+          for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, v[k][u]);
+          acc = add_rn<T>(p, acc);
+        }
+      }
+      for (; j < E; ++j) {
+        T p = ins[0][off[0] + j * sin[0]];
+        for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k] + j * sin[k]]);
+        acc = add_rn<T>(p, acc);
+      }
+      // odometer over the outer reduction axes (last of them fastest)
+      for (int a = n_red - 2; a >= 0; --a) {
         const int ax = n_par + a;
         if (++idx[a] < d.extents[ax]) {
           for (int k = 0; k < n_in; ++k) off[k] += d.strides[k][ax];
