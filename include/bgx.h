@@ -117,7 +117,8 @@ BGX_API int bgx_generic(const bgx_generic_desc *d, void *stream);
  *                    accumulate); BGX_ERR_UNSUPPORTED if not TMA-legal.
  *   BGX_MODE_SIMT    CUDA-core path for any dtype (f32 accumulate for 16-bit).
  *   BGX_MODE_TF32    f32 inputs on the tensor cores (tcgen05 kind::tf32, f32
- *                    accumulate; 10-bit mantissa products, rel. err ~1e-3).
+ *                    accumulate; 10-bit mantissa products, rel. err ~1e-3);
+ *                    any operand majorness (MN-major via SWIZZLE_128B_BASE32B).
  * Output dtype may be the input dtype or f32 (out_dtype).  The TC path needs
  * one unit stride in each of a (k or m) and b (k or n), 16-byte aligned base
  * pointers and 16-byte multiple non-unit strides, and out/c0 n-stride 1.    */

@@ -309,13 +309,13 @@ __device__ __forceinline__ void tmem_ld_wait() {
 // SBO>>4 [32,46), version=1 [46,48), base_offset [49,52), layout [61,64)
 // with SWIZZLE_128B = 2.  Unit-tested on the host by tests/test_descriptors.py.
 __host__ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t saddr, uint32_t lbo,
-                                                              uint32_t sbo) {
+                                                              uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)(layout & 7u) << 61;   // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
   return d;
 }
 

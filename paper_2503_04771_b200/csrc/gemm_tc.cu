@@ -300,10 +300,17 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       // only the start-address field moves along K, so precompute the rest.
       // per-MMA K advance: 32 bytes along a K-major row, or MMA_K rows of 128 B
       // for MN-major; MN-major LBO = one box (MN_ATOM x BK), SBO = 8 rows
+      // 32-bit MN-major operands use the SWIZZLE_128B_BASE32B layout (32-byte
+      // chunks swizzled within 128 B, 4-row atoms: SBO = 512 B) — the TMA map
+      // of such operands uses CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B to match.
       constexpr uint32_t MN_STEP = E::MMA_K * ROW_BYTES;
+      constexpr uint32_t MN_LAYOUT = IN_BYTES == 4 ? 1u : 2u;
+      constexpr uint32_t MN_SBO = IN_BYTES == 4 ? 512u : 1024u;
       const uint32_t a_step = (p.a_mn ? MN_STEP : 32u) >> 4, b_step = (p.b_mn ? MN_STEP : 32u) >> 4;
-      const uint64_t a_fixed = make_sdesc_sw128(0, p.a_mn ? (uint32_t)E::BOX_BYTES : 16u, 1024);
-      const uint64_t b_fixed = make_sdesc_sw128(0, p.b_mn ? (uint32_t)E::BOX_BYTES : 16u, 1024);
+      const uint64_t a_fixed = p.a_mn ? make_sdesc_sw128(0, E::BOX_BYTES, MN_SBO, MN_LAYOUT)
+                                      : make_sdesc_sw128(0, 16u, 1024);
+      const uint64_t b_fixed = p.b_mn ? make_sdesc_sw128(0, E::BOX_BYTES, MN_SBO, MN_LAYOUT)
+                                      : make_sdesc_sw128(0, 16u, 1024);
       const uint32_t sa0 = smem_u32(smem_a) >> 4, sb0 = smem_u32(smem_b) >> 4;
       // With a single 512-column accumulator (BN = 512) the two N = 256 halves
       // are released separately by the epilogue (tmem_empty[0] = columns
@@ -591,13 +598,17 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   CUtensorMap ma, mb;
   int rc;
   constexpr uint32_t AT = E::MN_ATOM, KB = E::BK;
+  const CUtensorMapSwizzle mn_swz =
+      IN_BYTES == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   if (p.a_mn)
-    rc = make_map(&ma, d.a, dt, d.M, d.K, d.batch, d.a_stride[2], d.a_stride[0], AT, KB, IN_BYTES);
+    rc = make_map(&ma, d.a, dt, d.M, d.K, d.batch, d.a_stride[2], d.a_stride[0], AT, KB, IN_BYTES,
+                  mn_swz);
   else
     rc = make_map(&ma, d.a, dt, d.K, d.M, d.batch, d.a_stride[1], d.a_stride[0], KB, BM, IN_BYTES);
   if (rc) return rc;
   if (p.b_mn)
-    rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], AT, KB, IN_BYTES);
+    rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], AT, KB, IN_BYTES,
+                  mn_swz);
   else
     rc = make_map(&mb, d.b, dt, d.K, d.N, d.batch, d.b_stride[2], d.b_stride[0], KB, C::B_BOX_N,
                   IN_BYTES);
@@ -712,10 +723,7 @@ bool tc_legal(const bgx_contract_desc &d, const char **why) {
     return fail("inputs not bf16/f16 (or f32 with BGX_MODE_TF32)");
   if (!(d.out_dtype == d.in_dtype || d.out_dtype == BGX_F32)) return fail("out dtype");
   const int es = tf32 ? 4 : 2;
-  // MN-major 32-bit operands need the SWIZZLE_128B_BASE32B UMMA layout (not
-  // implemented): tf32 takes K-major A and B; callers transpose otherwise.
-  if (tf32 && (d.a_stride[2] != 1 || (d.b_stride[1] != 1 && !(d.K == 1))))
-    return fail("tf32 needs K-major A and B (k unit stride)");
+
   if (d.M <= 0 || d.N <= 0 || d.K <= 0 || d.batch <= 0) return fail("empty extent");
   if (d.M >= (1ll << 31) || d.N >= (1ll << 31) || d.K >= (1ll << 31)) return fail("extent >= 2^31");
   const bool a_mn = d.a_stride[2] != 1 && d.a_stride[1] == 1;

@@ -123,8 +123,8 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
     """One ``bgx_contract`` call on raw (tensor, 3 strides) views; returns the
     kernel id that ran (_lib.KERNEL_*)."""
     lib = _lib.load()
-    if mode == "tf32":
-        # the tf32 kernel takes K-major operands: materialise others once
+    if mode == "tf32" and schedule and schedule.get("tf32_kmajor"):
+        # optional: materialise MN-major operands K-major first (comparison path)
         if a_strides[2] != 1 and K > 1:
             a3 = torch.as_strided(a, (batch, M, K), a_strides)
             a = permute(a3, torch.empty((batch, M, K), dtype=a.dtype, device=a.device), (0, 1, 2))
@@ -147,7 +147,7 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
     d.mode = MODES[mode]
     if schedule:
         for k, v in schedule.items():
-            if k in ("splits", "no_splitk"):
+            if k in ("splits", "no_splitk", "tf32_kmajor"):
                 continue
             if k == "reserved":
                 for i, x in enumerate(v):
