@@ -51,9 +51,10 @@ struct Params {
   int64_t tiles_m, tiles_n;
 };
 
-constexpr int TM = 4, TN = 4, BK = 16;
+constexpr int BK = 16;
 
-template <typename In, typename Out, typename Acc, bool FUSED, int BM, int BN>
+template <typename In, typename Out, typename Acc, bool FUSED, int BM, int BN, int TM = 4,
+          int TN = 4>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 simt_gemm_kernel(const Params p) {
   constexpr int NT = (BM / TM) * (BN / TN);
@@ -230,8 +231,15 @@ int launch(const bgx_contract_desc &d, cudaStream_t s) {
     p.sc[i] = d.c_stride[i]; p.so[i] = d.o_stride[i];
   }
   const int sms = sm_count_current();
-  const bool small = (d.M * d.N * d.batch) < (int64_t)sms * 64 * 64 * 2;
-  if (small) {
+  const int64_t outs = d.M * d.N * d.batch;
+  const bool small = outs < (int64_t)sms * 64 * 64 * 2;
+  if (outs <= (int64_t)sms * 2048) {
+    // latency-bound sizes: one output per thread, 16 x 16 tiles (the per-output
+    // k-sequential chain is the floor, so maximise the number of chains)
+    p.tiles_m = (d.M + 15) / 16; p.tiles_n = (d.N + 15) / 16;
+    int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
+    simt_gemm_kernel<In, Out, Acc, FUSED, 16, 16, 1, 1><<<(unsigned)blocks, 256, 0, s>>>(p);
+  } else if (small) {
     p.tiles_m = (d.M + 31) / 32; p.tiles_n = (d.N + 31) / 32;
     int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
     simt_gemm_kernel<In, Out, Acc, FUSED, 32, 32><<<(unsigned)blocks, 64, 0, s>>>(p);
