@@ -249,6 +249,11 @@ def _direct_gemm(a, b, out, batch=1):
     d.in_dtype = d.out_dtype = _lib.BF16
     d.mode = _lib.MODE_TC
     sp = torch.cuda.current_stream().cuda_stream
+    splits, ws_bytes = _lib._i32(1), _lib._i64(0)
+    lib.bgx_contract_splitk_plan(d, splits, ws_bytes)
+    if splits.value != 1:   # (tail) split-K as the library plans it; workspace preallocated
+        ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=out.device)
+        return lambda: lib.bgx_contract_splitk(d, splits.value, ws.data_ptr(), ws_bytes.value, sp)
     return lambda: lib.bgx_contract(d, sp)
 
 

@@ -165,8 +165,11 @@ BGX_API int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group, in
  * output, long K): `splits` persistent units per tile each contract a K slice
  * on the tensor cores into f32 partials in `workspace` (splits x batch x M x N
  * floats), then one reduction kernel sums the slices in order, adds c0 and
- * casts.  bgx_contract_splitk_plan returns the split count the library would
- * use (1 = not worth it) and the workspace size in bytes.                  */
+ * casts.  splits < -1 selects the TAIL split instead (stream-K style): full
+ * waves of tiles run unsplit and only the tiles of the last, partial wave are
+ * split into -splits K slices (f32 partials in `workspace`, then a fix-up
+ * kernel).  bgx_contract_splitk_plan returns the split count the library
+ * would use (1 = neither is worth it) and the workspace size in bytes.     */
 BGX_API int bgx_contract_splitk_plan(const bgx_contract_desc *d, int32_t *splits,
                                      int64_t *workspace_bytes);
 BGX_API int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, void *workspace,

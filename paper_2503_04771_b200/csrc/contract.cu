@@ -138,7 +138,7 @@ extern "C" int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, v
   int rc = validate(*d);
   if (rc) return rc;
   if (d->batch == 0 || d->M == 0 || d->N == 0) return BGX_OK;
-  if (splits <= 1 || d->K == 0) return bgx_contract(d, stream);
+  if ((splits <= 1 && splits >= -1) || d->K == 0) return bgx_contract(d, stream);
   const int kind = select_kind(*d);
   if (kind != KIND_TC) {
     set_error("bgx_contract_splitk: split-K runs on the tensor-core path only");

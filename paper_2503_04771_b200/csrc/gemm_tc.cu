@@ -58,6 +58,13 @@ struct TcParams {
   int64_t num_tiles;
   int32_t k_splits, kb_per_split;  // split-K: unit u -> tile u % num_tiles, K slice u / num_tiles
   int64_t num_units;
+  // tail split (stream-K style): tiles >= tail_start are split into
+  // tail_splits K slices whose f32 partials go to `ws` (one dense
+  // TILE_M x BN block per slice) and are reduced by tail_fixup_kernel
+  int64_t tail_start;
+  int32_t tail_splits, kb_per_tail;
+  float *ws;
+  int64_t ws_bytes;
   uint32_t idesc;
   int32_t a_mn, b_mn;            // 1 = MN-major operand
   int32_t stages;                // ring depth actually used (<= Cfg::STAGES)
@@ -139,6 +146,35 @@ __device__ __forceinline__ void stage_row32(uint8_t *buf, int r, const float *v)
       *reinterpret_cast<uint4 *>(buf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) = pk;
     }
   }
+}
+
+struct UnitInfo {
+  int64_t t;       // tile index
+  int kb_lo, nkb;  // K-block range
+  int64_t slot;    // >= 0: tail-split partial slot in ws; -1: regular output
+  int64_t kslice;  // uniform split-K slice (extra output batch), else 0
+};
+__device__ __forceinline__ UnitInfo unit_info(const TcParams &p, int64_t u) {
+  UnitInfo r;
+  r.slot = -1;
+  r.kslice = 0;
+  if (p.tail_splits > 1 && u >= p.tail_start) {
+    const int64_t tt = p.num_tiles - p.tail_start;
+    const int64_t v = u - p.tail_start;
+    r.t = p.tail_start + v % tt;
+    const int s = (int)(v / tt);
+    r.kb_lo = s * p.kb_per_tail;
+    const int hi = r.kb_lo + p.kb_per_tail < p.k_blocks ? r.kb_lo + p.kb_per_tail : p.k_blocks;
+    r.nkb = hi - r.kb_lo;
+    r.slot = s * tt + (r.t - p.tail_start);
+    return r;
+  }
+  r.t = u % p.num_tiles;
+  r.kslice = u / p.num_tiles;
+  r.kb_lo = (int)r.kslice * p.kb_per_split;
+  const int hi = r.kb_lo + p.kb_per_split < p.k_blocks ? r.kb_lo + p.kb_per_split : p.k_blocks;
+  r.nkb = hi - r.kb_lo;
+  return r;
 }
 
 template <typename OutT> struct Store;
@@ -249,9 +285,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t u = cluster_id; u < p.num_units; u += num_clusters) {
-      const int64_t t = u % p.num_tiles;
-      const int kb_lo = (int)(u / p.num_tiles) * p.kb_per_split;
-      const int kb_hi = kb_lo + p.kb_per_split < p.k_blocks ? kb_lo + p.kb_per_split : p.k_blocks;
+      const UnitInfo ui = unit_info(p, u);
+      const int64_t t = ui.t;
+      const int kb_lo = ui.kb_lo, kb_hi = ui.kb_lo + ui.nkb;
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
       const int32_t m0 = (int32_t)(tm * C::TILE_M + rank * BM);
@@ -334,8 +370,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         else umma_commit_mc(&empty[st], 0x3);
       };
       for (int64_t u = cluster_id; u < p.num_units; u += num_clusters, ++it) {
-        const int kb_lo = (int)(u / p.num_tiles) * p.kb_per_split;
-        const int nkb = (kb_lo + p.kb_per_split < p.k_blocks ? kb_lo + p.kb_per_split : p.k_blocks) - kb_lo;
+        const int nkb = unit_info(p, u).nkb;
         const int acc = it % C::ACC_BUFS;
         const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -399,10 +434,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     uint8_t *ebuf = smem_epi + ew * 2 * C::EPI_BUF_BYTES;
     int it = 0, chunk = 0;
     for (int64_t u = cluster_id; u < p.num_units; u += num_clusters, ++it) {
-      const int64_t t = u % p.num_tiles;
+      const UnitInfo ui = unit_info(p, u);
+      const int64_t t = ui.t;
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
-      b += (u / p.num_tiles) * p.batch;  // split-K slices are extra output batches
+      b += ui.kslice * p.batch;  // uniform split-K slices are extra output batches
+      // tail-split partial: dense f32 block of the workspace for this slice
+      float *wsrow = ui.slot >= 0 ? p.ws + ui.slot * (int64_t)C::TILE_M * BN +
+                                        (int64_t)(rank * BM + quad * 32 + lane) * BN
+                                  : nullptr;
       const int acc = it % C::ACC_BUFS;
       const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
@@ -490,11 +530,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         const int64_t valid = p.N - n;
-        if (crow && row_ok) {
+        if (crow && row_ok && wsrow == nullptr) {
           for (int j = 0; j < 32; ++j)
             if (j < valid) v[j] = __fadd_rn(v[j], Conv<OutT>::to_f(crow[n + j]));
         }
-        if (p.tma_store) {
+        if (wsrow != nullptr) {
+          Store<float>::row32(wsrow + c * 32, v, true, 32);
+        } else if (p.tma_store) {
           uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
           ++chunk;
           if (lane == 0) bulk_wait_read<1>();   // the buffer used two chunks ago is free
@@ -587,6 +629,29 @@ int max_clusters(K kern, int smem, int cg) {
   return n;
 }
 
+// out = c0 + sum over K slices of the tail tiles' f32 partials (slices in order)
+template <typename OutT>
+__global__ void __launch_bounds__(256)
+tail_fixup_kernel(const TcParams p, int tile_m, int bn) {
+  const int64_t tt = p.num_tiles - p.tail_start;
+  const int64_t per_tile = (int64_t)tile_m * bn;
+  const int64_t total = tt * per_tile;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ti = i / per_tile, e = i % per_tile;
+    const int64_t r = e / bn, c = e % bn;
+    int64_t b, tm, tn;
+    tile_coords(p, p.tail_start + ti, b, tm, tn);
+    const int64_t m = tm * tile_m + r, n = tn * bn + c;
+    if (m >= p.M || n >= p.N) continue;
+    float v = 0.f;
+    for (int sl = 0; sl < p.tail_splits; ++sl) v = __fadd_rn(v, p.ws[(sl * tt + ti) * per_tile + e]);
+    if (p.c0)
+      v = __fadd_rn(v, Conv<OutT>::to_f(static_cast<const OutT *>(p.c0)[b * p.sc[0] + m * p.sc[1] + n * p.sc[2]]));
+    static_cast<OutT *>(p.out)[b * p.so[0] + m * p.so[1] + n * p.so[2]] = Conv<OutT>::from_f(v);
+  }
+}
+
 template <int BN, int CG, typename OutT, int IN_BYTES>
 int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   using C = Cfg<BN, CG, (int)sizeof(OutT), IN_BYTES>;
@@ -653,6 +718,24 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
     if (clusters[dev & 63] <= 0) clusters[dev & 63] = sm_count_current() / CG;
   }
   int64_t nclusters = clusters[dev & 63];
+  // tail split: only the tiles of the last, partial wave are split in K
+  if (p.tail_splits > 1 && p.k_splits == 1 && C::ACC_BUFS == 2 && p.ws != nullptr) {
+    const int64_t slots = nclusters;
+    p.tail_start = (p.num_tiles / slots) * slots;
+    const int64_t tt = p.num_tiles - p.tail_start;
+    p.kb_per_tail = (p.k_blocks + p.tail_splits - 1) / p.tail_splits;
+    p.tail_splits = (p.k_blocks + p.kb_per_tail - 1) / p.kb_per_tail;
+    const int64_t need = tt * p.tail_splits * (int64_t)C::TILE_M * BN * 4;
+    if (tt == 0 || p.tail_splits < 2 || need > p.ws_bytes) {
+      p.tail_splits = 1;
+      p.tail_start = p.num_tiles;
+    } else {
+      p.num_units = p.tail_start + tt * p.tail_splits;
+    }
+  } else {
+    p.tail_splits = 1;
+    p.tail_start = p.num_tiles;
+  }
   if (p.num_units < nclusters) nclusters = p.num_units;
   if (d.sched.max_ctas > 0 && nclusters * CG > d.sched.max_ctas) nclusters = d.sched.max_ctas / CG;
   if (nclusters < 1) nclusters = 1;
@@ -669,7 +752,13 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   BGX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, p));
-  return check_launch("tc_gemm_kernel");
+  int rc2 = check_launch("tc_gemm_kernel");
+  if (rc2 || p.tail_splits <= 1) return rc2;
+  const int64_t total = (p.num_tiles - p.tail_start) * (int64_t)C::TILE_M * BN;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > (int64_t)sm_count_current() * 8) blocks = (int64_t)sm_count_current() * 8;
+  tail_fixup_kernel<OutT><<<(unsigned)blocks, 256, 0, s>>>(p, C::TILE_M, BN);
+  return check_launch("tail_fixup_kernel");
 }
 
 template <int CG, typename OutT, int IB = 2>
@@ -746,7 +835,8 @@ bool tc_legal(const bgx_contract_desc &d, const char **why) {
 void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out);
 
 namespace {
-int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s) {
+int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s, int tail_splits = 1,
+                     void *ws = nullptr, int64_t ws_bytes = 0) {
   const char *why = nullptr;
   if (!tc_legal(d, &why)) {
     set_error("tensor-core path not legal: %s", why);
@@ -754,6 +844,9 @@ int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s) {
   }
   TcParams p{};
   p.k_splits = splits;
+  p.tail_splits = tail_splits;
+  p.ws = static_cast<float *>(ws);
+  p.ws_bytes = ws_bytes;
   p.batch = d.batch; p.M = d.M; p.N = d.N; p.K = d.K;
   p.a_mn = d.a_stride[2] != 1 ? 1 : 0;
   p.b_mn = d.b_stride[2] == 1 ? 1 : 0;
@@ -811,7 +904,21 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
   const int64_t slots = sm_count_current() / cg;
   const int BKe = d.in_dtype == BGX_F32 ? Elem<4>::BK : Elem<2>::BK;
   const int64_t k_blocks = (d.K + BKe - 1) / BKe;
-  if (tiles * 2 > slots || k_blocks < 16) return;
+  if (tiles * 2 > slots || k_blocks < 16) {
+    // tail split: when the last wave is less than 3/4 full, split only its
+    // tiles in K (reported as a negative split count)
+    // (measured on B200: at K = 4096 the partial-tile stores + fix-up cost
+    // more than the saved half wave — 1091 vs 1430 TFLOP/s on 4096^3 — so the
+    // automatic plan only uses it for long K; schedule {"splits": -S} forces it)
+    const int64_t tail = tiles % slots;
+    if (bn > 256 || tiles < slots || tail == 0 || tail * 4 > slots * 3 || k_blocks < 512) return;
+    int64_t ts = slots / tail;
+    if (ts > 4) ts = 4;
+    if (ts < 2) return;
+    *splits = -(int)ts;
+    *ws_bytes = (slots - 1) * ts * (int64_t)(128 * cg) * bn * 4;
+    return;
+  }
   int64_t sp = slots / tiles;
   if (sp > k_blocks / 8) sp = k_blocks / 8;
   if (sp > 32) sp = 32;
@@ -822,6 +929,10 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
 
 int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t ws_bytes,
                        cudaStream_t s) {
+  if (splits < -1) {  // tail split of the last partial wave
+    BGX_CHECK_ARG(ws != nullptr && ((uintptr_t)ws % 16) == 0, "tail split: workspace must be 16B aligned");
+    return contract_tc_impl(d, 1, s, -splits, ws, ws_bytes);
+  }
   if (splits <= 1) return contract_tc(d, s);
   BGX_CHECK_ARG(ws != nullptr && ((uintptr_t)ws % 16) == 0, "split-K: workspace must be 16B aligned");
   BGX_CHECK_ARG(ws_bytes >= (int64_t)splits * d.batch * d.M * d.N * 4,

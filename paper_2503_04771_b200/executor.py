@@ -162,13 +162,16 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
         _lib.check(lib.bgx_contract_splitk_plan(d, splits, ws_bytes), "bgx_contract_splitk_plan")
         if schedule and schedule.get("splits"):
             splits.value = int(schedule["splits"])
-            ws_bytes.value = splits.value * batch * M * N * 4
+            if splits.value < -1:   # forced tail split: upper-bound workspace
+                ws_bytes.value = lib.bgx_sm_count() * -splits.value * 256 * 256 * 4
+            else:
+                ws_bytes.value = splits.value * batch * M * N * 4
     with torch.cuda.device(out.device):
-        if splits.value > 1:
+        if splits.value > 1 or splits.value < -1:
             ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=out.device)
             _lib.check(lib.bgx_contract_splitk(d, splits.value, ws.data_ptr(), ws_bytes.value,
                                                _stream_ptr(out)), "bgx_contract_splitk")
-            _log("tcgen05-splitk")
+            _log("tcgen05-splitk" if splits.value > 1 else "tcgen05-tailsplit")
             return kind
         _lib.check(lib.bgx_contract(d, _stream_ptr(out)), "bgx_contract")
     _log(_lib.KERNEL_NAMES.get(kind, "contract"))
