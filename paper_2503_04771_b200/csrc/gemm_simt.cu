@@ -132,7 +132,7 @@ simt_gemm_kernel(const Params p) {
 constexpr int BT = 128, BKB = 8;
 
 template <typename In, typename Out, typename Acc, bool FUSED>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, sizeof(Acc) == 4 ? 2 : 1)
 simt_gemm_big_kernel(const Params p) {
   __shared__ __align__(16) Acc As[2][BKB][BT];
   __shared__ __align__(16) Acc Bs[2][BKB][BT];
@@ -151,22 +151,76 @@ simt_gemm_big_kernel(const Params p) {
   const int a_r = a_k ? tid / 2 : (tid % 32) * 4, a_c = a_k ? (tid % 2) * 4 : tid / 32;
   const int b_r = b_n ? tid / 32 : (tid % 2) * 4, b_c = b_n ? (tid % 32) * 4 : tid / 2;
   Acc ra[4], rb[4];
+  // 16-byte vector loads when the 4 elements a thread fetches are contiguous
+  // and aligned (f32 operands with unit inner stride); scalar otherwise
+  const bool vec_a = sizeof(In) == 4 && sizeof(Acc) == 4 &&
+                     (a_k ? (p.sa[1] % 4 == 0 && p.K % 4 == 0) : (p.sa[2] % 4 == 0 && p.M % 4 == 0)) &&
+                     p.sa[0] % 4 == 0 && ((uintptr_t)p.a % 16) == 0;
+  const bool vec_b = sizeof(In) == 4 && sizeof(Acc) == 4 &&
+                     (b_n ? (p.sb[1] % 4 == 0 && p.N % 4 == 0) : (p.sb[2] % 4 == 0 && p.K % 4 == 0)) &&
+                     p.sb[0] % 4 == 0 && ((uintptr_t)p.b % 16) == 0 &&
+                     (b_n ? p.sb[2] == 1 : p.sb[1] == 1);
+  // per-thread operand pointers at k = 0; each k-tile advances them by BKB * k-stride
+  const In *pa = A + (int64_t)(m0 + (a_k ? a_r : a_r)) * p.sa[1] + (int64_t)a_c * p.sa[2];
+  const In *pb = B + (int64_t)(b_r) * p.sb[1] + (int64_t)(n0 + b_c) * p.sb[2];
+  const int64_t a_kstep = (int64_t)BKB * p.sa[2], b_kstep = (int64_t)BKB * p.sb[1];
+  const int64_t a_qstep = a_k ? p.sa[2] : p.sa[1];   // between the 4 elements of a thread
+  const int64_t b_qstep = b_n ? p.sb[2] : p.sb[1];
+  const int64_t a_m = m0 + a_r, b_n0 = n0 + b_c;
   auto load_tiles = [&](int64_t k0) {
+    const int64_t ak = k0 + a_c, bk = k0 + b_r;
+    if (vec_a) {
+      if (a_m < p.M && ak < p.K) {
+        const float4 v = *reinterpret_cast<const float4 *>(pa);
+        ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
+      } else {
+        ra[0] = ra[1] = ra[2] = ra[3] = (Acc)0;
+      }
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int mm = a_k ? a_r : a_r + q, kk = a_k ? a_c + q : a_c;
-      const int64_t m = m0 + mm, k = k0 + kk;
-      ra[q] = (m < p.M && k < p.K) ? to_acc<In, Acc>(A[m * p.sa[1] + k * p.sa[2]]) : (Acc)0;
-      const int kb_ = b_n ? b_r : b_r + q, nn = b_n ? b_c + q : b_c;
-      const int64_t kb2 = k0 + kb_, n = n0 + nn;
-      rb[q] = (n < p.N && kb2 < p.K) ? to_acc<In, Acc>(B[kb2 * p.sb[1] + n * p.sb[2]]) : (Acc)0;
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = a_k ? (a_m < p.M && ak + q < p.K) : (a_m + q < p.M && ak < p.K);
+        ra[q] = ok ? to_acc<In, Acc>(pa[q * a_qstep]) : (Acc)0;
+      }
     }
+    if (vec_b) {
+      if (bk < p.K && b_n0 < p.N) {
+        const float4 v = *reinterpret_cast<const float4 *>(pb);
+        rb[0] = v.x; rb[1] = v.y; rb[2] = v.z; rb[3] = v.w;
+      } else {
+        rb[0] = rb[1] = rb[2] = rb[3] = (Acc)0;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = b_n ? (bk < p.K && b_n0 + q < p.N) : (bk + q < p.K && b_n0 < p.N);
+        rb[q] = ok ? to_acc<In, Acc>(pb[q * b_qstep]) : (Acc)0;
+      }
+    }
+    pa += a_kstep;
+    pb += b_kstep;
   };
   auto store_tiles = [&](int buf) {
+    // contiguous-in-tile fragments go out as one 16-byte store (no conflicts)
+    if constexpr (sizeof(Acc) == 4) {
+      if (!a_k) {
+        *reinterpret_cast<float4 *>(&As[buf][a_c][a_r]) = make_float4(ra[0], ra[1], ra[2], ra[3]);
+      } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (a_k) As[buf][a_c + q][a_r] = ra[q]; else As[buf][a_c][a_r + q] = ra[q];
-      if (b_n) Bs[buf][b_r][b_c + q] = rb[q]; else Bs[buf][b_r + q][b_c] = rb[q];
+        for (int q = 0; q < 4; ++q) As[buf][a_c + q][a_r] = ra[q];
+      }
+      if (b_n) {
+        *reinterpret_cast<float4 *>(&Bs[buf][b_r][b_c]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Bs[buf][b_r + q][b_c] = rb[q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (a_k) As[buf][a_c + q][a_r] = ra[q]; else As[buf][a_c][a_r + q] = ra[q];
+        if (b_n) Bs[buf][b_r][b_c + q] = rb[q]; else Bs[buf][b_r + q][b_c] = rb[q];
+      }
     }
   };
   Acc acc[8][8];
