@@ -19,6 +19,7 @@ ap.add_argument("--stages", default="0")
 ap.add_argument("--raster", default="0")
 ap.add_argument("--debug", default="0")
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--batch", type=int, default=1)
 args = ap.parse_args()
 lib = _lib.load()
 dev = torch.device("cuda", 0)
@@ -27,17 +28,18 @@ flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 
 for shape in args.shapes.split(","):
     M, N, K = (int(x) for x in shape.split("x"))
-    a = torch.randn(M, K, device=dev).bfloat16()
-    b = torch.randn(K, N, device=dev).bfloat16()
-    out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    Bt = args.batch
+    a = torch.randn(Bt, M, K, device=dev).bfloat16()
+    b = torch.randn(Bt, K, N, device=dev).bfloat16()
+    out = torch.empty(Bt, M, N, device=dev, dtype=torch.bfloat16)
     for cg, bn, st, ra, dbg in itertools.product(*(map(int, v.split(",")) for v in
                                                    (args.cg, args.bn, args.stages, args.raster, args.debug))):
         d = _lib.BgxContractDesc()
-        d.batch, d.M, d.N, d.K = 1, M, N, K
+        d.batch, d.M, d.N, d.K = Bt, M, N, K
         d.a, d.b, d.out = a.data_ptr(), b.data_ptr(), out.data_ptr()
-        d.a_stride[:] = [0, K, 1]
-        d.b_stride[:] = [0, N, 1]
-        d.o_stride[:] = [0, N, 1]
+        d.a_stride[:] = [M * K, K, 1]
+        d.b_stride[:] = [K * N, N, 1]
+        d.o_stride[:] = [M * N, N, 1]
         d.in_dtype = d.out_dtype = _lib.BF16
         d.mode = _lib.MODE_TC
         d.sched.cta_group, d.sched.tile_n, d.sched.stages, d.sched.raster = cg, bn, st, ra
@@ -56,4 +58,4 @@ for shape in args.shapes.split(","):
         torch.cuda.synchronize()
         ms = statistics.median(x.elapsed_time(y) for x, y in ts)
         print(f"{shape} cg={cg} bn={bn} stages={st} raster={ra} debug={dbg}: {ms:.4f} ms "
-              f"{2 * M * N * K / ms / 1e9:.1f} TFLOP/s", flush=True)
+              f"{2 * Bt * M * N * K / ms / 1e9:.1f} TFLOP/s", flush=True)
