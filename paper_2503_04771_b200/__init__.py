@@ -11,6 +11,7 @@ Multi-GPU: ``shard``.  Kernels: libbgx.so (C ABI in include/bgx.h).
 from . import einsum, interp  # noqa: F401
 from .api import contract, contract_host  # noqa: F401
 from .prepared import Prepared, prepare  # noqa: F401
+from .schedule import Schedule  # noqa: F401
 from .einsum import (BF16, F16, F32, F64, EinsumError, EinsumSpec,  # noqa: F401
                      build_einsum_function, derive_maps, parse_einsum)
 from .interp import (DEFAULT_STEP_LIMIT, InterpError, StepLimitExceeded,  # noqa: F401

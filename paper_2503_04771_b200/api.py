@@ -32,16 +32,19 @@ def output_shape(spec: EinsumSpec, operands) -> tuple:
 
 def contract(spec, *operands: torch.Tensor, out: torch.Tensor | None = None,
              c0: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
-             mode: str = "auto", schedule: dict | None = None,
+             mode: str = "auto", schedule=None,
              chain_order: str = "left") -> torch.Tensor:
     """Evaluate an einsum spec such as ``"(i,k),(k,j)->(i,j)"`` on CUDA tensors.
 
     ``c0``: initial output (the reference's output operand; None = zeros).
     ``out``: optional preallocated result (may alias nothing else).
     ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt' (include/bgx.h).
+    ``schedule``: optional ``Schedule`` / dict / ``"tile_n=512,cta_group=2"``.
     ``chain_order``: 'left' or 'optimal' pairwise order for 3+ inputs."""
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
+    from .schedule import as_schedule_dict
+    schedule = as_schedule_dict(schedule)
     if len(operands) != len(spec.inputs):
         raise ValueError(f"expected {len(spec.inputs)} input(s), got {len(operands)}")
     shape = output_shape(spec, operands)

@@ -36,6 +36,7 @@ import torch
 
 from . import executor
 from .einsum import EinsumSpec
+from .schedule import as_schedule_dict
 
 _saved = {}
 
@@ -122,7 +123,10 @@ def _generic_b200(self, op, env):
     dev = torch.device("cuda", torch.cuda.current_device())
     tens = [torch.from_numpy(np.ascontiguousarray(v.data)).to(dev) for v in operands]
     res = torch.empty(tuple(out.data.shape), dtype=tens[-1].dtype, device=dev)
-    executor.execute(spec, tens[:-1], tens[-1], res, mode=_saved.get("mode", "auto"))
+    sched_attr = op.attributes.get("bgx.schedule")
+    sched = as_schedule_dict(getattr(sched_attr, "text", sched_attr)) if sched_attr else None
+    executor.execute(spec, tens[:-1], tens[-1], res, mode=_saved.get("mode", "auto"),
+                     schedule=sched)
     result = res.cpu().numpy()
     env[op.results[0]] = interp.TensorValue(out.elem, result.shape, result)
     return None

@@ -211,10 +211,14 @@ class GenericOp:
     operands: list
     results: list = field(default_factory=list)
     name: str = "linalg.generic"
+    schedule: object = None   # schedule.Schedule (transform-style tiling parameters)
 
     @property
     def attributes(self):
-        return {"indexing_maps": self.maps, "iterator_types": self.iterators}
+        attrs = {"indexing_maps": self.maps, "iterator_types": self.iterators}
+        if self.schedule is not None:
+            attrs["bgx.schedule"] = str(self.schedule)
+        return attrs
 
 
 @dataclass(eq=False)
@@ -256,10 +260,12 @@ class FunctionBuilder:
         self.function.result_types = [v.type for v in values]
 
 
-def build_generic(ctx: FunctionBuilder, registry, spec: EinsumSpec, operands) -> GenericOp:
+def build_generic(ctx: FunctionBuilder, registry, spec: EinsumSpec, operands,
+                  schedule=None) -> GenericOp:
     """One ``linalg.generic``; ``operands`` = input tensors then the output
     (einsum.py:121-161, same checks and messages).  ``registry`` is accepted
-    for signature compatibility and unused."""
+    for signature compatibility and unused.  ``schedule`` (optional
+    ``schedule.Schedule`` or its string form) pins the kernel variant."""
     if len(operands) != len(spec.inputs) + 1:
         raise EinsumError(
             f"expected {len(spec.inputs)} input(s) plus one output operand, "
@@ -279,20 +285,23 @@ def build_generic(ctx: FunctionBuilder, registry, spec: EinsumSpec, operands) ->
             raise EinsumError("operands must share one element type")
     maps, iterators = derive_maps(spec)
     op = GenericOp(spec, maps, iterators, body_ops(spec), elem, list(operands))
+    if schedule is not None:
+        from .schedule import Schedule
+        op.schedule = schedule if isinstance(schedule, Schedule) else Schedule.parse(str(schedule))
     op.results = [Value(operands[-1].type)]
     ctx.append(op)
     return op
 
 
 def build_einsum_function(registry, spec: EinsumSpec, elem=F32,
-                          symbol: str = "einsum") -> Module:
+                          symbol: str = "einsum", schedule=None) -> Module:
     """``func.func @symbol(inputs…, out) -> out_type`` holding one generic
     (einsum.py:164-191)."""
     e = elem_type(elem)
     module = Module()
     types = [TensorType(e, len(t)) for t in (*spec.inputs, spec.output)]
     ctx = FunctionBuilder(module, symbol, types)
-    op = build_generic(ctx, registry, spec, list(ctx.arguments))
+    op = build_generic(ctx, registry, spec, list(ctx.arguments), schedule=schedule)
     ctx.ret([op.results[0]])
     return module
 
@@ -314,9 +323,10 @@ def print_module(module: Module) -> str:
             ins, out = op.operands[:-1], op.operands[-1]
             maps = ", ".join(str(m) for m in op.maps)
             its = ", ".join(f'"{s}"' for s in op.iterators)
+            sched = f', bgx.schedule = "{op.schedule}"' if op.schedule is not None else ""
             lines.append(
                 f"    {rname} = linalg.generic {{indexing_maps = [{maps}], "
-                f"iterator_types = [{its}]}} ins({', '.join(names[id(v)] for v in ins)} : "
+                f"iterator_types = [{its}]{sched}}} ins({', '.join(names[id(v)] for v in ins)} : "
                 f"{', '.join(str(v.type) for v in ins)}) outs({names[id(out)]} : {out.type}) {{")
             bargs = [f"%{next(counter)}" for _ in op.operands]
             e = op.elem

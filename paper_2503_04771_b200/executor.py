@@ -40,6 +40,16 @@ def launch_log() -> list:
 
 def reset_launch_log():
     _trace.log = []
+    _trace.tiles = []
+
+
+def tile_log() -> list:
+    """(cta_group, tile_n, splits) of each tcgen05 launch made under an
+    explicit schedule since the last ``reset_launch_log`` — how a
+    ``Schedule`` attached to a generic op is observed to take effect."""
+    if not hasattr(_trace, "tiles"):
+        _trace.tiles = []
+    return _trace.tiles
 
 
 def _log(name: str):
@@ -166,6 +176,10 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
                 ws_bytes.value = lib.bgx_sm_count() * -splits.value * 256 * 256 * 4
             else:
                 ws_bytes.value = splits.value * batch * M * N * 4
+    if schedule and kind == _lib.KERNEL_TC:
+        cg, bn = _lib._i32(0), _lib._i32(0)
+        _lib.check(lib.bgx_contract_tile(d, cg, bn), "bgx_contract_tile")
+        tile_log().append((cg.value, bn.value, splits.value))
     with torch.cuda.device(out.device):
         if splits.value > 1 or splits.value < -1:
             ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=out.device)

@@ -29,6 +29,7 @@ import torch
 
 from . import executor
 from .einsum import BF16, F16, F32, F64, ElemType, Module, TensorType, elem_type
+from .schedule import as_schedule_dict
 
 __all__ = ["InterpError", "StepLimitExceeded", "DEFAULT_STEP_LIMIT", "TensorValue",
            "run_function"]
@@ -161,8 +162,9 @@ def run_function(module: Module, symbol: str, inputs, step_limit=DEFAULT_STEP_LI
         tensors = [device_of(v) for v in op.operands]
         out_t = torch.empty(tuple(vals[-1].dims), dtype=_TORCH[op.elem], device=device)
         with torch.cuda.device(device):
+            sched = as_schedule_dict(op.schedule if op.schedule is not None else schedule)
             executor.execute(op.spec, tensors[:-1], tensors[-1], out_t, mode=mode,
-                             schedule=schedule)
+                             schedule=sched)
         res = op.results[0]
         env[id(res)] = TensorValue(op.elem, tuple(out_t.shape), out_t)
         dev[id(res)] = out_t

@@ -33,7 +33,9 @@ class Prepared:
                  mode: str = "auto", schedule=None, chain_order: str = "left",
                  graph: bool = False):
         self.spec = spec if isinstance(spec, EinsumSpec) else parse_einsum(spec)
-        self.mode, self.schedule, self.chain_order = mode, schedule, chain_order
+        from .schedule import as_schedule_dict
+        self.mode, self.chain_order = mode, chain_order
+        self.schedule = as_schedule_dict(schedule)
         dt = out_dtype or tensors[0].dtype
         if out is None:
             out = torch.empty(output_shape(self.spec, tensors), dtype=dt, device=tensors[0].device)

@@ -85,3 +85,20 @@ class TestReferenceEinsumSuite:
         text = E.print_module(E.build_einsum_function(None, parse_einsum("(i,k),(k,j)->(i,j)"),
                                                       elem=E.BF16))
         assert "tensor<?x?xbf16>" in text and "arith.mulf %1, %2 : bf16" in text
+
+
+def test_schedule_attribute_roundtrip():
+    from paper_2503_04771_b200.schedule import Schedule, as_schedule_dict
+    s = Schedule.parse("tile_n=512, cta_group=2")
+    assert s == Schedule(tile_n=512, cta_group=2) and str(s) == "tile_n=512,cta_group=2"
+    assert as_schedule_dict("raster=-8") == {"raster": -8}
+    with pytest.raises(ValueError, match="unknown schedule parameter"):
+        Schedule.parse("tiles=3")
+    mod = E.build_einsum_function(None, parse_einsum("(i,k),(k,j)->(i,j)"), elem=E.BF16,
+                                  schedule="tile_n=256,cta_group=1")
+    op = mod.lookup_symbol("einsum").ops[0]
+    assert op.attributes["bgx.schedule"] == "tile_n=256,cta_group=1"
+    assert 'bgx.schedule = "tile_n=256,cta_group=1"' in E.print_module(mod)
+    # without a schedule the printed text stays the reference's
+    plain = E.print_module(E.build_einsum_function(None, parse_einsum("(i,k),(k,j)->(i,j)")))
+    assert plain == G.printed_cases()["(i,k),(k,j)->(i,j)|f32"]
