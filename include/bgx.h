@@ -175,6 +175,57 @@ BGX_API int bgx_contract_splitk_plan(const bgx_contract_desc *d, int32_t *splits
 BGX_API int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, void *workspace,
                                 int64_t workspace_bytes, void *stream);
 
+/* ---- multi-GPU K-split: GEMM fused with the reduce-scatter ----------------
+ * Replaces the K-split exchange (per-rank K slab -> f32 partials
+ * -> ncclReduceScatter -> cast) by ONE tcgen05 kernel per rank whose
+ * epilogue moves the partial tiles over NVLink as they finish:
+ *   level 1 (only when local_splits > 1): the rank's K slab is split again
+ *     over its SMs; each unit stores its f32 tile to the local `ws`
+ *     (local_splits x M x N) and bumps ws_counters[tile]; the last local
+ *     unit sums the slices in slice order and carries on with level 2;
+ *   level 2: the rank's f32 partial tile is stored straight into the owner's
+ *     slot  slots[owner] + (rank * rows_per_owner + local_row) * N  (peer
+ *     memory: plain st.global over NVLink) and, after a system-scope fence,
+ *     counters[owner][tile] is bumped with a system-scope atomic; the unit
+ *     that brings it to `world` sums the world slots IN RANK ORDER (bitwise
+ *     deterministic, independent of arrival order), adds c0[owner], casts to
+ *     out_dtype and stores the owner's output rows.
+ * Output row r belongs to owner r / rows_per_owner (a multiple of the tile
+ * height); out[owner]/c0[owner] point at that owner's rows_per_owner x N
+ * slab (row strides desc.o_stride[1] / desc.c_stride[1]).  No rank ever waits
+ * for another inside the kernel (the last arriver does the work), so the
+ * kernel cannot deadlock; the caller orders consecutive calls with a barrier
+ * (slots are reused).  Counters must be zero before the first call; each call
+ * leaves them zero.  desc.a/b are the rank's K slab (M x K_r, K_r x N);
+ * desc.out/c0 are ignored; batch must be 1.  On one GPU, `world` launches
+ * with local buffers (rank 0..world-1 in stream order) compute exactly what
+ * `world` GPUs would.  bgx_contract_rs_plan fills tile shape, rows_per_owner,
+ * local_splits and the buffer sizes for a (M, N, K_r, world) problem; every
+ * rank must use the same plan.                                              */
+#define BGX_MAX_RANKS 8
+typedef struct {
+  int32_t world, rank;
+  int32_t cta_group, tile_n;     /* tile shape (from the plan)               */
+  int32_t local_splits;          /* >= 1                                     */
+  int32_t out_dtype;             /* bgx_dtype of out / c0                    */
+  int64_t rows_per_owner;
+  int64_t slot_bytes;            /* per owner: world * rows_per_owner * N * 4 */
+  int64_t counter_bytes;         /* per owner and for ws_counters            */
+  int64_t ws_bytes;              /* local: local_splits * M * N * 4 (or 0)   */
+} bgx_rs_plan;
+typedef struct {
+  bgx_rs_plan plan;
+  float *slots[BGX_MAX_RANKS];            /* per owner, peer-mapped         */
+  uint32_t *counters[BGX_MAX_RANKS];      /* per owner, peer-mapped         */
+  void *out[BGX_MAX_RANKS];               /* per owner, peer-mapped         */
+  const void *c0[BGX_MAX_RANKS];          /* per owner or NULL              */
+  float *ws;                              /* local (local_splits > 1)       */
+  uint32_t *ws_counters;                  /* local                          */
+} bgx_reduce_scatter;
+BGX_API int bgx_contract_rs_plan(const bgx_contract_desc *d, int32_t world, bgx_rs_plan *plan);
+BGX_API int bgx_contract_reduce_scatter(const bgx_contract_desc *d, const bgx_reduce_scatter *rs,
+                                        void *stream);
+
 /* ---- elementwise helpers for multi-GPU K-split -------------------------
  * out[i] = (dtype_out) src[i] for n elements, src f32 (the reduced partials),
  * out f32/bf16/f16; with c0 != NULL adds c0[i] first (in f32).           */

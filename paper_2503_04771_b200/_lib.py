@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libbgx.so")
 MAX_RANK = 8
 MAX_AXES = 12
 MAX_OPERANDS = 6
+MAX_RANKS = 8
 
 # bgx_dtype
 F32, F64, BF16, F16 = 0, 1, 2, 3
@@ -62,6 +63,18 @@ class BgxContractDesc(ctypes.Structure):
                 ("sched", BgxSchedule)]
 
 
+class BgxRsPlan(ctypes.Structure):
+    _fields_ = [("world", _i32), ("rank", _i32), ("cta_group", _i32), ("tile_n", _i32),
+                ("local_splits", _i32), ("out_dtype", _i32), ("rows_per_owner", _i64),
+                ("slot_bytes", _i64), ("counter_bytes", _i64), ("ws_bytes", _i64)]
+
+
+class BgxReduceScatter(ctypes.Structure):
+    _fields_ = [("plan", BgxRsPlan), ("slots", _vp * MAX_RANKS), ("counters", _vp * MAX_RANKS),
+                ("out", _vp * MAX_RANKS), ("c0", _vp * MAX_RANKS), ("ws", _vp),
+                ("ws_counters", _vp)]
+
+
 # name -> (restype, argtypes): exactly the functions include/bgx.h declares
 SIGNATURES = {
     "bgx_version": (ctypes.c_int, []),
@@ -78,6 +91,10 @@ SIGNATURES = {
                                                 ctypes.POINTER(_i32), ctypes.POINTER(_i64)]),
     "bgx_contract_splitk": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc), _i32, _vp, _i64,
                                            _vp]),
+    "bgx_contract_rs_plan": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc), _i32,
+                                            ctypes.POINTER(BgxRsPlan)]),
+    "bgx_contract_reduce_scatter": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
+                                                   ctypes.POINTER(BgxReduceScatter), _vp]),
     "bgx_cast_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _vp]),
     "bgx_rtc_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p,
                                        ctypes.POINTER(_vp), ctypes.c_char_p, _i64]),

@@ -9,6 +9,8 @@ void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out);
 void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes);
 int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t ws_bytes,
                        cudaStream_t s);
+int tc_rs_plan(const bgx_contract_desc &d, int world, bgx_rs_plan *pl);
+int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cudaStream_t s);
 
 namespace {
 
@@ -147,4 +149,21 @@ extern "C" int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, v
   BGX_CHECK_ARG(d->a != nullptr && d->b != nullptr && d->out != nullptr,
                 "bgx_contract_splitk: null operand");
   return contract_tc_splitk(*d, splits, workspace, workspace_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int bgx_contract_rs_plan(const bgx_contract_desc *d, int32_t world, bgx_rs_plan *plan) {
+  BGX_CHECK_ARG(d && plan, "bgx_contract_rs_plan: null argument");
+  int rc = validate(*d);
+  if (rc) return rc;
+  return tc_rs_plan(*d, world, plan);
+}
+
+extern "C" int bgx_contract_reduce_scatter(const bgx_contract_desc *d, const bgx_reduce_scatter *rs,
+                                           void *stream) {
+  BGX_CHECK_ARG(d && rs, "bgx_contract_reduce_scatter: null argument");
+  int rc = validate(*d);
+  if (rc) return rc;
+  BGX_CHECK_ARG(d->M > 0 && d->N > 0 && d->K > 0, "bgx_contract_reduce_scatter: empty extent");
+  BGX_CHECK_ARG(d->a != nullptr && d->b != nullptr, "bgx_contract_reduce_scatter: null operand");
+  return contract_tc_rs(*d, *rs, (cudaStream_t)stream);
 }

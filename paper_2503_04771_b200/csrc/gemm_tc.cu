@@ -72,6 +72,14 @@ struct TcParams {
   int32_t debug;                 // bit 0: skip the epilogue stores (timing probe)
   const void *c0; int64_t sc[3];
   void *out; int64_t so[3];
+  // fused K-split reduce-scatter epilogue (RS kernels only, bgx.h)
+  int32_t rs_world, rs_rank, rs_out_dtype;
+  int64_t rs_rpo;                       // output rows per owner
+  float *rs_slots[BGX_MAX_RANKS];
+  uint32_t *rs_counters[BGX_MAX_RANKS];
+  void *rs_out[BGX_MAX_RANKS];
+  const void *rs_c0[BGX_MAX_RANKS];
+  uint32_t *rs_ws_counters;
 };
 
 template <int BN, int CG, int OUT_BYTES, int IN_BYTES = 2> struct Cfg {
@@ -212,6 +220,47 @@ template <typename H> struct Store16 {
 template <> struct Store<__nv_bfloat16> : Store16<__nv_bfloat16> {};
 template <> struct Store<__half> : Store16<__half> {};
 
+// ---- fused K-split reduce-scatter epilogue helpers --------------------------
+
+// 32 f32 values of a row written by another CTA or GPU in this kernel.
+__device__ __forceinline__ void load_row32_sys(const float *src, float *v, int64_t valid) {
+  if (valid >= 32 && ((uintptr_t)src & 15) == 0) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 q = ld_sys_v4(src + j);
+      v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+    }
+  } else {
+    for (int j = 0; j < 32; ++j) v[j] = j < valid ? ld_sys(src + j) : 0.f;
+  }
+}
+
+// Publish this CTA's stores for one tile and count the arrival on `counter`
+// (system scope when the counter and the data may live on another GPU).
+// Returns true in every epilogue thread of the unit that completes the
+// count (it resets the counter for the next call).  No thread ever waits for
+// another CTA or GPU: the last arriver does the reduction.
+template <bool SYS>
+__device__ __forceinline__ bool rs_arrive(uint32_t *counter, uint32_t target, int *flag,
+                                          int nthreads) {
+  if (SYS) __threadfence_system(); else __threadfence();
+  named_bar_sync(1, nthreads);
+  if (threadIdx.x == 128) {   // first epilogue thread
+    const uint32_t old = SYS ? atomicAdd_system(counter, 1u) : atomicAdd(counter, 1u);
+    const int last = old == target - 1;
+    if (last) {
+      if (SYS) atomicExch_system(counter, 0u); else atomicExch(counter, 0u);
+    }
+    *flag = last;
+  }
+  named_bar_sync(1, nthreads);
+  const bool last = *(volatile int *)flag != 0;
+  if (last) {
+    if (SYS) __threadfence_system(); else __threadfence();
+  }
+  return last;
+}
+
 template <int CG>
 __device__ __forceinline__ void tma_load(void *dst, const void *tmap, uint64_t *bar, int32_t c0,
                                          int32_t c1, int32_t c2) {
@@ -219,7 +268,7 @@ __device__ __forceinline__ void tma_load(void *dst, const void *tmap, uint64_t *
   else tma_load_3d_cg2(dst, tmap, bar, c0, c1, c2);
 }
 
-template <int BN, int CG, typename OutT, int IN_BYTES>
+template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                const __grid_constant__ CUtensorMap tmap_b,
@@ -241,6 +290,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   uint64_t *tmem_full = bars + 2 * MAX_STAGES;
   uint64_t *tmem_empty = bars + 2 * MAX_STAGES + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * MAX_STAGES + 4);
+  int *rs_flag = reinterpret_cast<int *>(tmem_slot + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -464,10 +514,105 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int64_t m_warp = tm * C::TILE_M + rank * BM + quad * 32;
       const int64_t m = m_warp + lane;
       const bool row_ok = m < p.M;
-      OutT *orow = static_cast<OutT *>(p.out) + b * p.so[0] + m * p.so[1];
-      const OutT *crow = p.c0 ? static_cast<const OutT *>(p.c0) + b * p.sc[0] + m * p.sc[1] : nullptr;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
       constexpr int NCHUNK = BN / 32;
+      if constexpr (RS) {
+        // ===== fused K-split reduce-scatter (bgx_contract_reduce_scatter) =====
+        // owner of this tile's rows and the row inside the owner's slab
+        const int owner = (int)((tm * C::TILE_M) / p.rs_rpo);
+        const int64_t lrow = m - (int64_t)owner * p.rs_rpo;
+        const int64_t cidx = t * CG + rank;   // one counter per CTA half of a tile
+        const int S = p.k_splits;
+        float *slot_row = p.rs_slots[owner] + ((int64_t)p.rs_rank * p.rs_rpo + lrow) * p.N;
+        float *dst = S > 1 ? p.ws + (ui.kslice * p.M + m) * p.N : slot_row;
+        // (1) TMEM -> f32 partial rows (local split slice, or straight into
+        //     the owner's slot over NVLink)
+        uint32_t rbuf[2][32];
+        tmem_ld_32x32b_x32(taddr + g * 32, rbuf[0]);
+#pragma unroll 1
+        for (int c = g, k = 0; c < NCHUNK; c += 2, ++k) {
+          tmem_ld_wait();
+          uint32_t (&r)[32] = rbuf[k & 1];
+          if (c + 2 < NCHUNK) tmem_ld_32x32b_x32(taddr + (c + 2) * 32, rbuf[(k + 1) & 1]);
+          const int64_t n = tn * BN + c * 32;
+          if (n >= p.N || !row_ok) continue;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          Store<float>::row32(dst + n, v, p.N - n >= 32, p.N - n);
+        }
+        tmem_ld_wait();
+        arrive_empty(acc);
+        constexpr int NT = 32 * EPI_WARPS;
+        // (2) local split-K: the last slice of this tile sums the slices in
+        //     slice order and forwards the rank's partial to the owner
+        if (S > 1) {
+          if (!rs_arrive<false>(p.rs_ws_counters + cidx, (uint32_t)S, rs_flag, NT)) continue;
+          if (row_ok) {
+#pragma unroll 1
+            for (int c = g; c < NCHUNK; c += 2) {
+              const int64_t n = tn * BN + c * 32;
+              if (n >= p.N) continue;
+              const int64_t valid = p.N - n;
+              float v[32], w[32];
+              load_row32_sys(p.ws + m * p.N + n, v, valid);
+              for (int sl = 1; sl < S; ++sl) {
+                load_row32_sys(p.ws + ((int64_t)sl * p.M + m) * p.N + n, w, valid);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], w[j]);
+              }
+              Store<float>::row32(slot_row + n, v, valid >= 32, valid);
+            }
+          }
+        }
+        // (3) cross-rank: the last rank to deliver this tile reduces the
+        //     owner's slots in rank order, adds c0 and writes the output
+        if (!rs_arrive<true>(p.rs_counters[owner] + cidx, (uint32_t)p.rs_world, rs_flag, NT))
+          continue;
+        if (row_ok) {
+          const float *slot0 = p.rs_slots[owner] + lrow * p.N;
+          const int64_t slot_stride = p.rs_rpo * p.N;
+          const int oes = p.rs_out_dtype == BGX_F32 ? 4 : 2;
+          uint8_t *orow_rs = static_cast<uint8_t *>(p.rs_out[owner]) + lrow * p.so[1] * oes;
+          const uint8_t *crow_rs = p.rs_c0[owner]
+              ? static_cast<const uint8_t *>(p.rs_c0[owner]) + lrow * p.sc[1] * oes : nullptr;
+#pragma unroll 1
+          for (int c = g; c < NCHUNK; c += 2) {
+            const int64_t n = tn * BN + c * 32;
+            if (n >= p.N) continue;
+            const int64_t valid = p.N - n;
+            float v[32], w[32];
+            load_row32_sys(slot0 + n, v, valid);
+            for (int rk = 1; rk < p.rs_world; ++rk) {
+              load_row32_sys(slot0 + rk * slot_stride + n, w, valid);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], w[j]);
+            }
+            if (p.rs_out_dtype == BGX_F32) {
+              if (crow_rs)
+                for (int j = 0; j < 32; ++j)
+                  if (j < valid) v[j] = __fadd_rn(v[j], ld_sys((const float *)crow_rs + n + j));
+              Store<float>::row32((float *)orow_rs + n, v, valid >= 32, valid);
+            } else if (p.rs_out_dtype == BGX_BF16) {
+              if (crow_rs)
+                for (int j = 0; j < 32; ++j)
+                  if (j < valid)
+                    v[j] = __fadd_rn(v[j], Conv<__nv_bfloat16>::to_f(
+                                               ((const __nv_bfloat16 *)crow_rs)[n + j]));
+              Store<__nv_bfloat16>::row32((__nv_bfloat16 *)orow_rs + n, v, valid >= 32, valid);
+            } else {
+              if (crow_rs)
+                for (int j = 0; j < 32; ++j)
+                  if (j < valid)
+                    v[j] = __fadd_rn(v[j], Conv<__half>::to_f(((const __half *)crow_rs)[n + j]));
+              Store<__half>::row32((__half *)orow_rs + n, v, valid >= 32, valid);
+            }
+          }
+        }
+        continue;
+      } else {
+      OutT *orow = static_cast<OutT *>(p.out) + b * p.so[0] + m * p.so[1];
+      const OutT *crow = p.c0 ? static_cast<const OutT *>(p.c0) + b * p.sc[0] + m * p.sc[1] : nullptr;
       if constexpr (SPLIT_RELEASE && sizeof(OutT) == 2) {
         if (p.tma_store && crow == nullptr && !(p.debug & 1)) {
           // Two-phase drain: read this warp's chunks of each accumulator half
@@ -554,6 +699,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       }
       tmem_ld_wait();
       arrive_empty(SPLIT_RELEASE ? 1 : acc);
+      }  // !RS
     }
     if (lane == 0) bulk_wait_all();
     __syncwarp();
@@ -652,7 +798,7 @@ tail_fixup_kernel(const TcParams p, int tile_m, int bn) {
   }
 }
 
-template <int BN, int CG, typename OutT, int IN_BYTES>
+template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false>
 int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   using C = Cfg<BN, CG, (int)sizeof(OutT), IN_BYTES>;
   using E = typename C::E;
@@ -685,7 +831,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   const int oes = (int)sizeof(OutT);
   p.tma_store = ((uintptr_t)d.out % 16 == 0) && (d.o_stride[1] * oes) % 16 == 0 &&
                 (d.batch * (p.k_splits > 1 ? p.k_splits : 1) <= 1 ||
-                 (d.o_stride[0] * oes) % 16 == 0) && !(p.debug & 2);
+                 (d.o_stride[0] * oes) % 16 == 0) && !(p.debug & 2) && !RS;
   if (p.tma_store) {
     const CUtensorMapDataType odt = oes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : (d.out_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
@@ -705,7 +851,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   p.num_units = p.num_tiles * p.k_splits;
-  auto kern = tc_gemm_kernel<BN, CG, OutT, IN_BYTES>;
+  auto kern = tc_gemm_kernel<BN, CG, OutT, IN_BYTES, RS>;
   static thread_local int configured[64] = {0};
   static thread_local int clusters[64] = {0};
   int dev = 0;
@@ -973,6 +1119,102 @@ int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t
           d.o_stride[2]);
   }
   return check_launch("splitk_reduce_kernel");
+}
+
+// ---- fused K-split reduce-scatter (bgx_contract_rs_plan / _reduce_scatter) ----
+
+int tc_rs_plan(const bgx_contract_desc &d, int world, bgx_rs_plan *pl) {
+  const char *why = nullptr;
+  BGX_CHECK_ARG(world >= 1 && world <= BGX_MAX_RANKS, "reduce-scatter: world %d", world);
+  BGX_CHECK_ARG(d.batch == 1, "reduce-scatter: batch must be 1 (got %lld)", (long long)d.batch);
+  BGX_CHECK_ARG(d.in_dtype == BGX_BF16 || d.in_dtype == BGX_F16,
+                "reduce-scatter: inputs must be bf16/f16");
+  BGX_CHECK_ARG(d.out_dtype == d.in_dtype || d.out_dtype == BGX_F32, "reduce-scatter: out dtype");
+  if (!tc_legal(d, &why)) {
+    set_error("tensor-core path not legal: %s", why);
+    return BGX_ERR_UNSUPPORTED;
+  }
+  memset(pl, 0, sizeof(*pl));
+  pl->world = world;
+  const int64_t rows = (d.M + world - 1) / world;
+  // CTA pairs (256-row tiles) when every owner's slab is a whole number of
+  // them (or large enough that rounding up wastes little), else 128-row tiles
+  const int cg = (rows % 256 == 0 || rows >= 2048) ? 2 : 1;
+  const int bn = d.N > 128 ? 256 : 128;
+  const int64_t tile_m = 128 * cg;
+  pl->cta_group = cg;
+  pl->tile_n = bn;
+  pl->rows_per_owner = (rows + tile_m - 1) / tile_m * tile_m;
+  const int64_t tiles = ((d.M + tile_m - 1) / tile_m) * ((d.N + bn - 1) / bn);
+  const int64_t slots = sm_count_current() / cg;
+  const int64_t k_blocks = (d.K + Elem<2>::BK - 1) / Elem<2>::BK;
+  int64_t sp = slots / (tiles > 0 ? tiles : 1);
+  if (sp > k_blocks / 8) sp = k_blocks / 8;
+  if (sp > 32) sp = 32;
+  if (sp < 1) sp = 1;
+  pl->local_splits = (int32_t)sp;
+  pl->out_dtype = d.out_dtype;
+  pl->slot_bytes = (int64_t)world * pl->rows_per_owner * d.N * 4;
+  pl->counter_bytes = (tiles * cg * 4 + 15) / 16 * 16;
+  pl->ws_bytes = sp > 1 ? sp * d.M * d.N * 4 : 0;
+  return BGX_OK;
+}
+
+int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cudaStream_t s) {
+  const bgx_rs_plan &pl = rs.plan;
+  const char *why = nullptr;
+  BGX_CHECK_ARG(pl.world >= 1 && pl.world <= BGX_MAX_RANKS && pl.rank >= 0 && pl.rank < pl.world,
+                "reduce-scatter: rank %d of %d", pl.rank, pl.world);
+  BGX_CHECK_ARG(d.batch == 1, "reduce-scatter: batch must be 1");
+  BGX_CHECK_ARG(d.in_dtype == BGX_BF16 || d.in_dtype == BGX_F16,
+                "reduce-scatter: inputs must be bf16/f16");
+  BGX_CHECK_ARG(pl.out_dtype == BGX_F32 || pl.out_dtype == d.in_dtype, "reduce-scatter: out dtype");
+  BGX_CHECK_ARG((pl.cta_group == 1 && (pl.tile_n == 128 || pl.tile_n == 256)) ||
+                    (pl.cta_group == 2 && pl.tile_n == 256),
+                "reduce-scatter: tile %d x %d", 128 * pl.cta_group, pl.tile_n);
+  const int64_t tile_m = 128 * pl.cta_group;
+  BGX_CHECK_ARG(pl.rows_per_owner > 0 && pl.rows_per_owner % tile_m == 0 &&
+                    pl.rows_per_owner * pl.world >= d.M,
+                "reduce-scatter: rows_per_owner %lld", (long long)pl.rows_per_owner);
+  BGX_CHECK_ARG(pl.local_splits >= 1 && (pl.local_splits == 1 || (rs.ws && rs.ws_counters)),
+                "reduce-scatter: local split workspace missing");
+  for (int r = 0; r < pl.world; ++r)
+    BGX_CHECK_ARG(rs.slots[r] && rs.counters[r] && rs.out[r],
+                  "reduce-scatter: null slot/counter/out pointer for owner %d", r);
+  bgx_contract_desc dd = d;
+  dd.out = nullptr;
+  dd.c0 = nullptr;
+  dd.sched.cta_group = pl.cta_group;
+  dd.sched.tile_n = pl.tile_n;
+  if (!tc_legal(dd, &why)) {
+    set_error("tensor-core path not legal: %s", why);
+    return BGX_ERR_UNSUPPORTED;
+  }
+  TcParams p{};
+  p.batch = 1; p.M = d.M; p.N = d.N; p.K = d.K;
+  p.a_mn = d.a_stride[2] != 1 ? 1 : 0;
+  p.b_mn = d.b_stride[2] == 1 ? 1 : 0;
+  p.k_blocks = (int32_t)((d.K + Elem<2>::BK - 1) / Elem<2>::BK);
+  p.k_splits = pl.local_splits > p.k_blocks ? p.k_blocks : pl.local_splits;
+  p.tail_splits = 1;
+  p.ws = rs.ws;
+  for (int i = 0; i < 3; ++i) { p.sc[i] = d.c_stride[i]; p.so[i] = d.o_stride[i]; }
+  p.raster = d.sched.raster != 0 ? d.sched.raster : (pl.cta_group == 2 ? 8 : 16);
+  p.debug = d.sched.reserved[0];
+  p.rs_world = pl.world;
+  p.rs_rank = pl.rank;
+  p.rs_out_dtype = pl.out_dtype;
+  p.rs_rpo = pl.rows_per_owner;
+  for (int r = 0; r < BGX_MAX_RANKS; ++r) {
+    p.rs_slots[r] = r < pl.world ? rs.slots[r] : nullptr;
+    p.rs_counters[r] = r < pl.world ? rs.counters[r] : nullptr;
+    p.rs_out[r] = r < pl.world ? rs.out[r] : nullptr;
+    p.rs_c0[r] = r < pl.world ? rs.c0[r] : nullptr;
+  }
+  p.rs_ws_counters = rs.ws_counters;
+  if (pl.cta_group == 2) return launch_tc<256, 2, float, 2, true>(dd, p, s);
+  if (pl.tile_n == 128) return launch_tc<128, 1, float, 2, true>(dd, p, s);
+  return launch_tc<256, 1, float, 2, true>(dd, p, s);
 }
 
 // Tile shape the TC path would use (bgx_contract_tile).

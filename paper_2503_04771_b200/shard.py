@@ -97,3 +97,192 @@ def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
     partial = contract(spec, a_slab, b_slab, out_dtype=torch.float32)
     return ksplit_reduce(partial, c0=c0, out_dtype=out_dtype or a_slab.dtype, group=group,
                          scatter=scatter)
+
+
+# ---------------------------------------------------------------------------
+# K-split fused with the reduce-scatter (bgx_contract_reduce_scatter)
+
+def _align(n: int, a: int = 256) -> int:
+    return (n + a - 1) // a * a
+
+
+def _rs_desc(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, out_dtype):
+    """bgx_contract_desc for this rank's K slab of a plain (batch-free) GEMM
+    spec; the output fields are unused by the fused kernel except the row
+    stride (dense slabs: N)."""
+    from .plan import GemmPlan, extents_of, plan_generic
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    ins = [a_slab, b_slab]
+    ext = extents_of(spec, [t.shape for t in ins])
+    oshape = tuple(ext[x] for x in spec.output)
+    ostride = tuple(int(s) for s in torch.empty(oshape, device="meta").stride())
+    p = plan_generic(spec, [tuple(t.shape) for t in ins] + [oshape],
+                     [tuple(t.stride()) for t in ins] + [ostride],
+                     dtype=executor.DTYPE_NAME[a_slab.dtype])
+    if not isinstance(p, GemmPlan) or p.batch != 1 or p.a_view.needs_copy or p.b_view.needs_copy:
+        raise ValueError(f"fused K-split needs a batch-free GEMM spec with strided operands: {spec}")
+    sa = executor._group_strides(ins[p.a], spec.inputs[p.a], p.a_view.axes, ext)
+    sb = executor._group_strides(ins[p.b], spec.inputs[p.b], p.b_view.axes, ext)
+    d = _lib.BgxContractDesc()
+    d.batch, d.M, d.N, d.K = 1, p.M, p.N, p.K
+    for i in range(3):
+        d.a_stride[i], d.b_stride[i] = sa[i], sb[i]
+    d.o_stride[0], d.o_stride[1], d.o_stride[2] = p.M * p.N, p.N, 1
+    d.c_stride[0], d.c_stride[1], d.c_stride[2] = p.M * p.N, p.N, 1
+    d.a, d.b = ins[p.a].data_ptr(), ins[p.b].data_ptr()
+    d.in_dtype = executor.TORCH_TO_BGX[a_slab.dtype]
+    d.out_dtype = executor.TORCH_TO_BGX[out_dtype]
+    d.mode = _lib.MODE_TC
+    return d, p
+
+
+def rs_plan(spec, a_slab, b_slab, world: int, out_dtype=None) -> _lib.BgxRsPlan:
+    """The fused kernel's plan (tile, rows per owner, local split, buffer
+    bytes) — identical on every rank for identical slab shapes."""
+    lib = _lib.load()
+    d, _ = _rs_desc(spec, a_slab, b_slab, out_dtype or a_slab.dtype)
+    pl = _lib.BgxRsPlan()
+    _lib.check(lib.bgx_contract_rs_plan(d, world, pl), "bgx_contract_rs_plan")
+    return pl
+
+
+def owned_rows(M: int, rows_per_owner: int, rank: int):
+    """Output rows [lo, hi) the fused reduce-scatter leaves on ``rank``."""
+    lo = min(M, rank * rows_per_owner)
+    return lo, min(M, lo + rows_per_owner)
+
+
+class FusedKSplit:
+    """K-split contraction whose reduce-scatter is fused into the tcgen05
+    GEMM epilogue (one kernel per rank; bgx.h ``bgx_contract_reduce_scatter``).
+
+    Each rank passes its K slab; partial tiles travel over NVLink into the
+    owner's symmetric-memory slot as they finish and the last contributor of
+    each tile reduces it (rank order, deterministic) into the owner's output
+    rows.  Peer buffers come from ``torch.distributed._symmetric_memory``
+    (world > 1); one device-side barrier before (slot reuse) and after (all of
+    this rank's rows delivered) each call.  ``__call__`` returns this rank's
+    ``owned_rows`` slab (a view of the symmetric buffer: valid until the next
+    call).  This replaces ``ksplit_contract(..., scatter=True)`` (GEMM ->
+    ``reduce_scatter_tensor`` -> cast) with no NCCL on the data path."""
+
+    def __init__(self, spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *, out_dtype=None,
+                 group=None, with_c0: bool = False):
+        self.spec = spec if isinstance(spec, EinsumSpec) else parse_einsum(spec)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.out_dtype = out_dtype or a_slab.dtype
+        self.dev = a_slab.device
+        self._lib = _lib.load()
+        d, p = _rs_desc(self.spec, a_slab, b_slab, self.out_dtype)
+        self.M, self.N = p.M, p.N
+        pl = _lib.BgxRsPlan()
+        _lib.check(self._lib.bgx_contract_rs_plan(d, self.world, pl), "bgx_contract_rs_plan")
+        pl.rank = self.rank
+        self.plan = pl
+        rpo, N = pl.rows_per_owner, self.N
+        esz = torch.tensor([], dtype=self.out_dtype).element_size()
+        regions = [("slots", pl.slot_bytes), ("counters", pl.counter_bytes),
+                   ("out", rpo * N * esz), ("c0", rpo * N * esz if with_c0 else 0)]
+        offs, total = {}, 0
+        for name, nbytes in regions:
+            offs[name] = total
+            total += _align(nbytes)
+        if dist.is_initialized() and self.dev.type == "cuda":
+            from torch.distributed import _symmetric_memory as symm_mem
+            self.buf = symm_mem.empty(total, dtype=torch.uint8, device=self.dev)
+            self.buf[offs["counters"]:offs["counters"] + pl.counter_bytes].zero_()
+            self.hdl = symm_mem.rendezvous(self.buf, self.group or dist.group.WORLD)
+            bases = list(self.hdl.buffer_ptrs)
+            self.hdl.barrier()
+        else:
+            self.buf = torch.zeros(total, dtype=torch.uint8, device=self.dev)
+            self.hdl = None
+            bases = [self.buf.data_ptr()]
+        rs = _lib.BgxReduceScatter()
+        rs.plan = pl
+        for r, base in enumerate(bases):
+            rs.slots[r] = base + offs["slots"]
+            rs.counters[r] = base + offs["counters"]
+            rs.out[r] = base + offs["out"]
+            rs.c0[r] = base + offs["c0"] if with_c0 else None
+        self.ws = None
+        if pl.local_splits > 1:
+            self.ws = torch.empty(pl.ws_bytes, dtype=torch.uint8, device=self.dev)
+            self.ws_counters = torch.zeros(max(16, pl.counter_bytes), dtype=torch.uint8,
+                                           device=self.dev)
+            rs.ws, rs.ws_counters = self.ws.data_ptr(), self.ws_counters.data_ptr()
+        self.rs = rs
+        self.desc = d
+        self._a_idx = p.a
+        lo, hi = owned_rows(self.M, rpo, self.rank)
+        o = offs["out"]
+        self.out = self.buf[o:o + rpo * N * esz].view(self.out_dtype).view(rpo, N)[:hi - lo]
+        self.c0_buf = (self.buf[offs["c0"]:offs["c0"] + rpo * N * esz].view(self.out_dtype)
+                       .view(rpo, N)[:hi - lo]) if with_c0 else None
+
+    def __call__(self, a_slab: torch.Tensor, b_slab: torch.Tensor, c0=None) -> torch.Tensor:
+        if (c0 is not None) != (self.c0_buf is not None):
+            raise ValueError("c0 must be given iff the FusedKSplit was built with_c0=True")
+        if c0 is not None:
+            self.c0_buf.copy_(c0)
+        ins = (a_slab, b_slab)
+        self.desc.a = ins[self._a_idx].data_ptr()
+        self.desc.b = ins[1 - self._a_idx].data_ptr()
+        if self.hdl is not None:
+            self.hdl.barrier()
+        _lib.check(self._lib.bgx_contract_reduce_scatter(
+            self.desc, self.rs, torch.cuda.current_stream(self.dev).cuda_stream),
+            "bgx_contract_reduce_scatter")
+        executor._log("tcgen05-rs")
+        if self.hdl is not None:
+            self.hdl.barrier()
+        return self.out
+
+
+def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> torch.Tensor:
+    """Run the fused K-split reduce-scatter of ``len(a_slabs)`` ranks on ONE
+    GPU: the same kernel, launched once per emulated rank in rank order, with
+    the owners' slots / counters / outputs as local buffers.  No launch waits
+    for another (the last contributor of each tile does the reduction), so
+    this is exactly the multi-GPU computation, serialised.  Returns the full
+    M x N output (the owners' slabs stacked)."""
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    world = len(a_slabs)
+    lib = _lib.load()
+    out_dtype = out_dtype or a_slabs[0].dtype
+    d, p = _rs_desc(spec, a_slabs[0], b_slabs[0], out_dtype)
+    pl = _lib.BgxRsPlan()
+    _lib.check(lib.bgx_contract_rs_plan(d, world, pl), "bgx_contract_rs_plan")
+    M, N, rpo = p.M, p.N, pl.rows_per_owner
+    dev = a_slabs[0].device
+    slots = torch.empty(world, pl.slot_bytes // 4, dtype=torch.float32, device=dev)
+    counters = torch.zeros(world, max(4, pl.counter_bytes // 4), dtype=torch.int32, device=dev)
+    out = torch.empty(world * rpo, N, dtype=out_dtype, device=dev)
+    c0_pad = None
+    if c0 is not None:
+        c0_pad = torch.zeros(world * rpo, N, dtype=out_dtype, device=dev)
+        c0_pad[:M].copy_(c0)
+    rs = _lib.BgxReduceScatter()
+    for r in range(world):
+        rs.slots[r] = slots[r].data_ptr()
+        rs.counters[r] = counters[r].data_ptr()
+        rs.out[r] = out[r * rpo].data_ptr()
+        rs.c0[r] = c0_pad[r * rpo].data_ptr() if c0_pad is not None else None
+    if pl.local_splits > 1:
+        ws = torch.empty(pl.ws_bytes, dtype=torch.uint8, device=dev)
+        wsc = torch.zeros(max(16, pl.counter_bytes), dtype=torch.uint8, device=dev)
+        rs.ws, rs.ws_counters = ws.data_ptr(), wsc.data_ptr()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    for r in range(world):
+        dr, pr = _rs_desc(spec, a_slabs[r], b_slabs[r], out_dtype)
+        if (pr.M, pr.N) != (M, N):
+            raise ValueError("all ranks' slabs must produce the same M x N output")
+        pl.rank = r
+        rs.plan = pl
+        _lib.check(lib.bgx_contract_reduce_scatter(dr, rs, stream), "bgx_contract_reduce_scatter")
+        executor._log("tcgen05-rs")
+    return out[:M]

@@ -53,6 +53,14 @@ def test_error_paths_without_gpu():
     g = _lib.BgxGenericDesc()
     g.n_in = 9
     assert lib.bgx_generic(g, None) == _lib.ERR_INVALID
+    d.in_dtype = d.out_dtype = _lib.BF16
+    pl = _lib.BgxRsPlan()
+    assert lib.bgx_contract_rs_plan(d, 9, pl) == _lib.ERR_INVALID
+    assert b"world 9" in lib.bgx_last_error()
+    rs = _lib.BgxReduceScatter()
+    rs.plan.world, rs.plan.rank = 2, 2
+    assert lib.bgx_contract_reduce_scatter(d, rs, None) == _lib.ERR_INVALID
+    assert b"null operand" in lib.bgx_last_error()
 
 
 @pytest.fixture(scope="module")
@@ -71,6 +79,10 @@ def test_struct_layouts(probe):
     assert probe["bgx_generic_desc"] == [ctypes.sizeof(G), G.ins.offset, G.c0.offset, G.out.offset]
     assert probe["bgx_contract_desc"] == [ctypes.sizeof(C), C.c0.offset, C.in_dtype.offset,
                                           C.sched.offset]
+    P, R = _lib.BgxRsPlan, _lib.BgxReduceScatter
+    assert probe["bgx_rs_plan"] == [ctypes.sizeof(P), P.rows_per_owner.offset, P.ws_bytes.offset]
+    assert probe["bgx_reduce_scatter"] == [ctypes.sizeof(R), R.slots.offset, R.out.offset,
+                                           R.ws.offset, R.ws_counters.offset]
 
 
 def sdesc(addr, lbo, sbo):
