@@ -190,8 +190,8 @@ BGX_API int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, void
  *     that brings it to `world` sums the world slots IN RANK ORDER (bitwise
  *     deterministic, independent of arrival order), adds c0[owner], casts to
  *     out_dtype and stores the owner's output rows.
- * Output row r belongs to owner r / rows_per_owner (a multiple of the tile
- * height); out[owner]/c0[owner] point at that owner's rows_per_owner x N
+ * Output row r belongs to owner r / rows_per_owner (a multiple of 128: a
+ * CTA pair's two 128-row halves may go to different owners); out[owner]/c0[owner] point at that owner's rows_per_owner x N
  * slab (row strides desc.o_stride[1] / desc.c_stride[1]).  No rank ever waits
  * for another inside the kernel (the last arriver does the work), so the
  * kernel cannot deadlock; the caller orders consecutive calls with a barrier

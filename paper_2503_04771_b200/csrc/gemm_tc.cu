@@ -518,8 +518,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       constexpr int NCHUNK = BN / 32;
       if constexpr (RS) {
         // ===== fused K-split reduce-scatter (bgx_contract_reduce_scatter) =====
-        // owner of this tile's rows and the row inside the owner's slab
-        const int owner = (int)((tm * C::TILE_M) / p.rs_rpo);
+        // owner of this CTA's 128 rows (rows_per_owner is a multiple of 128,
+        // so the two CTAs of a pair may deliver to different owners) and the
+        // row inside the owner's slab
+        const int owner = (int)((tm * C::TILE_M + rank * BM) / p.rs_rpo);
         const int64_t lrow = m - (int64_t)owner * p.rs_rpo;
         const int64_t cidx = t * CG + rank;   // one counter per CTA half of a tile
         const int S = p.k_splits;
@@ -919,24 +921,44 @@ int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStrea
   }
 }
 
+// Uniform split-K count for `tiles` output tiles on `slots` persistent
+// clusters: only when the tiles leave most clusters idle and every slice
+// keeps >= 8 k-blocks (shared by the tile choice and tc_splitk_plan).
+int64_t uniform_splits(int64_t tiles, int64_t slots, int64_t k_blocks) {
+  if (tiles * 2 > slots || k_blocks < 16) return 1;
+  int64_t sp = slots / tiles;
+  if (sp > k_blocks / 8) sp = k_blocks / 8;
+  if (sp > 32) sp = 32;
+  return sp < 2 ? 1 : sp;
+}
+
 // Tile choice: minimise waves x per-CTA tile area / efficiency over the
 // candidate (CG, BN) shapes.  A CTA's time per tile is proportional to its
 // tile area at the full per-SM MMA rate, scaled by the shape's measured
 // efficiency (round-1 sweeps on B200, scripts/sweep_gemm.py: narrower tiles
 // pay relatively more epilogue / A-operand traffic per flop, single CTAs more
-// L2->SM bytes of B).  A later candidate must be >3 % cheaper to win.
+// L2->SM bytes of B).  Small outputs are costed with the split-K they would
+// get (a unit is then 1/S of a tile's K, +10 % for the partial stores and
+// the reduction pass), so wide tiles split in K beat narrow unsplit ones.
+// A later candidate must be >3 % cheaper to win.
 void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
   struct Cand { int cg, bn; double eff; };
   const Cand cands[] = {{2, 512, 1.06}, {2, 256, 1.00}, {2, 128, 0.85}, {1, 256, 0.88},
                         {1, 128, 0.80}, {1, 64, 0.60}};
+  const int BKe = d.in_dtype == BGX_F32 ? Elem<4>::BK : Elem<2>::BK;
+  const int64_t k_blocks = (d.K + BKe - 1) / BKe;
   double best = -1.0;
   for (const Cand &c : cands) {
     if (c.bn > 64 && d.N <= c.bn / 2) continue;  // tiles would be mostly empty
     const int64_t tm = (d.M + 128 * c.cg - 1) / (128 * c.cg);
     const int64_t tn = (d.N + c.bn - 1) / c.bn;
     const int64_t slots = sms / c.cg;
-    const int64_t waves = (tm * tn * d.batch + slots - 1) / slots;
-    const double cost = (double)waves * (double)(128 * c.bn) / c.eff;
+    const int64_t tiles = tm * tn * d.batch;
+    const int64_t sp = uniform_splits(tiles, slots, k_blocks);
+    const int64_t waves = (tiles + slots - 1) / slots;
+    const int64_t split_waves = (tiles * sp + slots - 1) / slots;
+    const double cost = (double)split_waves * (double)(128 * c.bn) / c.eff / (double)sp *
+                        (sp > 1 ? 1.1 : 1.0);
     // single 512-column accumulator: its drain is amortised only over long K
     // and many waves (4096^3 measured faster with 256-wide tiles)
     if (c.bn == 512 && (d.N < 1024 || d.K < 8192 || waves < 8)) continue;
@@ -1050,7 +1072,8 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
   const int64_t slots = sm_count_current() / cg;
   const int BKe = d.in_dtype == BGX_F32 ? Elem<4>::BK : Elem<2>::BK;
   const int64_t k_blocks = (d.K + BKe - 1) / BKe;
-  if (tiles * 2 > slots || k_blocks < 16) {
+  const int64_t sp = uniform_splits(tiles, slots, k_blocks);
+  if (sp == 1) {
     // tail split: when the last wave is less than 3/4 full, split only its
     // tiles in K (reported as a negative split count)
     // (measured on B200: at K = 4096 the partial-tile stores + fix-up cost
@@ -1065,10 +1088,6 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
     *ws_bytes = (slots - 1) * ts * (int64_t)(128 * cg) * bn * 4;
     return;
   }
-  int64_t sp = slots / tiles;
-  if (sp > k_blocks / 8) sp = k_blocks / 8;
-  if (sp > 32) sp = 32;
-  if (sp < 2) return;
   *splits = (int)sp;
   *ws_bytes = sp * d.batch * d.M * d.N * 4;
 }
@@ -1137,14 +1156,14 @@ int tc_rs_plan(const bgx_contract_desc &d, int world, bgx_rs_plan *pl) {
   memset(pl, 0, sizeof(*pl));
   pl->world = world;
   const int64_t rows = (d.M + world - 1) / world;
-  // CTA pairs (256-row tiles) when every owner's slab is a whole number of
-  // them (or large enough that rounding up wastes little), else 128-row tiles
-  const int cg = (rows % 256 == 0 || rows >= 2048) ? 2 : 1;
+  // CTA pairs (256-row tiles); ownership is per CTA (128 rows), so each
+  // owner's slab only has to be a multiple of 128 rows
+  const int cg = d.M > 128 ? 2 : 1;
   const int bn = d.N > 128 ? 256 : 128;
   const int64_t tile_m = 128 * cg;
   pl->cta_group = cg;
   pl->tile_n = bn;
-  pl->rows_per_owner = (rows + tile_m - 1) / tile_m * tile_m;
+  pl->rows_per_owner = (rows + BM - 1) / BM * BM;
   const int64_t tiles = ((d.M + tile_m - 1) / tile_m) * ((d.N + bn - 1) / bn);
   const int64_t slots = sm_count_current() / cg;
   const int64_t k_blocks = (d.K + Elem<2>::BK - 1) / Elem<2>::BK;
@@ -1172,8 +1191,7 @@ int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cud
   BGX_CHECK_ARG((pl.cta_group == 1 && (pl.tile_n == 128 || pl.tile_n == 256)) ||
                     (pl.cta_group == 2 && pl.tile_n == 256),
                 "reduce-scatter: tile %d x %d", 128 * pl.cta_group, pl.tile_n);
-  const int64_t tile_m = 128 * pl.cta_group;
-  BGX_CHECK_ARG(pl.rows_per_owner > 0 && pl.rows_per_owner % tile_m == 0 &&
+  BGX_CHECK_ARG(pl.rows_per_owner > 0 && pl.rows_per_owner % BM == 0 &&
                     pl.rows_per_owner * pl.world >= d.M,
                 "reduce-scatter: rows_per_owner %lld", (long long)pl.rows_per_owner);
   BGX_CHECK_ARG(pl.local_splits >= 1 && (pl.local_splits == 1 || (rs.ws && rs.ws_counters)),

@@ -61,7 +61,7 @@ def test_plan_tiles_and_ownership(dev):
     a = torch.empty(1024, 2048, device=dev, dtype=torch.bfloat16)
     b = torch.empty(2048, 1024, device=dev, dtype=torch.bfloat16)
     pl = shard.rs_plan(MM, a, b, 8)
-    assert (pl.cta_group, pl.rows_per_owner) == (1, 128)
+    assert (pl.cta_group, pl.rows_per_owner) == (2, 128)
     pl2 = shard.rs_plan(MM, torch.empty(4096, 2048, device=dev, dtype=torch.bfloat16), b, 2)
     assert (pl2.cta_group, pl2.tile_n, pl2.rows_per_owner) == (2, 256, 2048)
     assert pl.local_splits >= 1 and pl.slot_bytes == 8 * 128 * 1024 * 4
