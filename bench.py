@@ -326,6 +326,46 @@ def aux_configs(dev, pk):
     return res
 
 
+def ksplit_aux(dev, world, rank):
+    """K-split contraction (SURVEY §8e demo shape: M = N = 1024, K = 2^18 per
+    rank, bf16) on every rank: the fused GEMM + reduce-scatter kernel
+    (shard.FusedKSplit: partial tiles delivered to the owner's symmetric-memory
+    slot from the GEMM epilogue) against the unfused baseline (tcgen05 GEMM to
+    an f32 partial -> NCCL reduce_scatter_tensor -> cast).  Device time, max
+    over ranks; TFLOP/s aggregate over ranks."""
+    from paper_2503_04771_b200 import shard
+    spec = "(i,k),(k,j)->(i,j)"
+    M = N = 1024
+    Kr = 1 << 18
+    g = torch.Generator(device=dev).manual_seed(11 + rank)
+    a = torch.randn(M, Kr, device=dev, generator=g).bfloat16()
+    b = torch.randn(Kr, N, device=dev, generator=g).bfloat16()
+    fused = shard.FusedKSplit(spec, a, b)
+    res = {"shape": {"M": M, "N": N, "K_per_rank": Kr, "world": world},
+           "plan": {"cta_group": fused.plan.cta_group, "tile_n": fused.plan.tile_n,
+                    "rows_per_owner": fused.plan.rows_per_owner,
+                    "local_splits": fused.plan.local_splits}}
+    flop = 2 * M * N * Kr * world
+    outs = {}
+    for name, fn in (("fused_rs", lambda: fused(a, b)),
+                     ("gemm_then_nccl_rs", lambda: shard.ksplit_contract(spec, a, b, scatter=True))):
+        for _ in range(3):
+            outs[name] = fn()
+        barrier_sync(world)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(10):
+            outs[name] = fn()
+        s1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(s0.elapsed_time(s1) / 10, world)
+        res[name] = {"ms": ms, "tflops": flop / ms / 1e9}
+    f, u = outs["fused_rs"].double(), outs["gemm_then_nccl_rs"].double()
+    res["relF_fused_vs_unfused"] = max_over_ranks(float((f - u).norm() / u.norm()), world)
+    res["speedup_fused"] = res["gemm_then_nccl_rs"]["ms"] / res["fused_rs"]["ms"]
+    return res
+
+
 def chain_optimal_order(dev):
     """Time-to-solution of the chain with the planner's min-flop order
     A @ (B @ C) (5.50 TFLOP executed instead of 8.80): the headline keeps the
@@ -474,9 +514,12 @@ def main():
 
     aux = None
     cpu = None
+    if not args.no_aux and (world == 1 or backend == "nccl"):
+        ks = ksplit_aux(dev, world, rank)
+        aux = {"ksplit_fused_reduce_scatter": ks}
     if rank == 0 and world == 1:
         if not args.no_aux:
-            aux = aux_configs(dev, pk)
+            aux.update(aux_configs(dev, pk))
             opt = chain_optimal_order(dev)
             opt["speedup_vs_left_to_right_time"] = ms / opt["ms"]
             aux["c5_chain_min_flop_order"] = opt
