@@ -52,3 +52,35 @@ def bits_equal(a, b) -> bool:
     b = np.asarray(b)
     return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(
         a.reshape(-1).view(np.uint8), b.reshape(-1).view(np.uint8))
+
+
+# ---- full-size BASELINE configs 1 and 2 (tests/golden/make_fullsize_golden.py)
+
+FULLSIZE_SPECS = {"c1": "(i,j),(j,k)->(i,k)", "c2a": "(i,j)->(j,i)", "c2b": "(i,j,k)->(k,j,i)"}
+
+
+def fullsize_inputs(config: str):
+    """The BASELINE inputs (standard_normal f32, seeds A = 1, B = 2)."""
+    if config == "c1":
+        a = np.random.default_rng(1).standard_normal((256, 256), dtype=np.float32)
+        b = np.random.default_rng(2).standard_normal((256, 256), dtype=np.float32)
+        return [a, b]
+    if config == "c2a":
+        return [np.random.default_rng(1).standard_normal((8192, 8192), dtype=np.float32)]
+    if config == "c2b":
+        return [np.random.default_rng(1).standard_normal((256, 512, 512), dtype=np.float32)]
+    raise KeyError(config)
+
+
+def fullsize_meta():
+    with open(os.path.join(GOLDEN, "fullsize_golden.json")) as fh:
+        return json.load(fh)
+
+
+def fullsize_c1():
+    return np.load(os.path.join(GOLDEN, "fullsize_c1.npz"))["out"]
+
+
+def sha256(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
