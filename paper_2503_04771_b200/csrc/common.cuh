@@ -126,13 +126,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+// The suspend-time hint lets a waiting warp sleep in hardware until the
+// phase completes (bounded by the hint, in ns) instead of re-polling: fewer
+// issued instructions while the pipeline is full, i.e. less power for the
+// same work on a power-capped part.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "BGX_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra BGX_WAIT_%=;\n\t}"
-      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+      ::"r"(smem_u32(bar)), "r"(parity), "r"(0x989680u) : "memory");
 }
 
 __device__ __forceinline__ void prefetch_tmap(const void *tmap) {
@@ -159,6 +163,20 @@ __device__ __forceinline__ void tma_load_3d_cg2(void *dst, const void *tmap, uin
       " [%0], [%1, {%3, %4, %5}], [%2];"
       ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
         "r"(c2)
+      : "memory");
+}
+
+// 2-CTA load multicast to the CTAs in `mask` (same smem offset in each);
+// the mbarrier address has the peer bit cleared, so every destination's
+// transaction bytes land on ITS pair leader's barrier.
+__device__ __forceinline__ void tma_load_3d_cg2_mc(void *dst, const void *tmap, uint64_t *bar,
+                                                   int32_t c0, int32_t c1, int32_t c2,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;"
+      ::"r"(smem_u32(dst)), "l"(tmap), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+        "r"(c2), "h"(mask)
       : "memory");
 }
 

@@ -268,7 +268,16 @@ __device__ __forceinline__ void tma_load(void *dst, const void *tmap, uint64_t *
   else tma_load_3d_cg2(dst, tmap, bar, c0, c1, c2);
 }
 
-template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false>
+// CN = 2 (CTA pairs only): a cluster of two pairs computes the two tiles
+// (tm, 2j) and (tm, 2j+1) of one schedule unit; both need the same A rows,
+// so each CTA loads HALF of its A k-block and multicasts it to its
+// counterpart in the other pair — L2->SM bytes per flop drop by 1/4 (1/6 for
+// 512-wide tiles), which on the power-capped B200 buys clock.  The A halves
+// are 2-CTA multicast loads whose bytes complete on each destination pair's
+// leader barrier, so full[s] still expects the pair's whole stage.  A stage
+// is refilled only after BOTH pairs' MMAs released it (empty[] counts CN
+// commits, multicast to all four CTAs).
+template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false, int CN = 1>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                const __grid_constant__ CUtensorMap tmap_b,
@@ -294,10 +303,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const uint32_t rank = CG == 1 ? 0 : cluster_ctarank();
+  static_assert(CN == 1 || (CG == 2 && IN_BYTES == 2 && !RS), "A multicast: CTA pairs, 16-bit");
+  constexpr int CL = CG * CN;                       // CTAs per cluster
+  const uint32_t crank = CL == 1 ? 0 : cluster_ctarank();
+  const uint32_t rank = crank & (uint32_t)(CG - 1); // rank inside the CTA pair
+  const uint32_t pair = CN == 1 ? 0 : crank >> 1;   // which pair of the cluster
+  const uint16_t pair_mask = (uint16_t)(0x3u << (2 * pair));
   const bool leader = rank == 0;
-  const int64_t cluster_id = blockIdx.x / CG;
-  const int64_t num_clusters = gridDim.x / CG;
+  const int64_t cluster_id = blockIdx.x / CL;
+  const int64_t num_clusters = gridDim.x / CL;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
@@ -305,7 +319,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     if (p.tma_store) prefetch_tmap(&tmap_o);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CN);   // one commit per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -318,7 +332,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     tmem_relinquish<CG>();
   }
   tc_fence_before();
-  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
+  if constexpr (CL == 1) __syncthreads(); else cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -340,6 +354,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int kb_lo = ui.kb_lo, kb_hi = ui.kb_lo + ui.nkb;
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
+      tn = tn * CN + pair;
       const int32_t m0 = (int32_t)(tm * C::TILE_M + rank * BM);
       // B columns of this CTA: for each MMA split h, [h*MMA_N + rank*B_BOX_N, +B_BOX_N)
       const int32_t n0 = (int32_t)(tn * BN + rank * C::B_BOX_N);
@@ -351,7 +366,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           const int32_t k0 = kb * BK;  // in elements
           uint8_t *sa = smem_a + stage * A_STAGE_BYTES;
           uint8_t *sb = smem_b + stage * C::B_STAGE_BYTES;
-          if (p.a_mn) {
+          if constexpr (CN == 2) {
+            // my half of the A rows, multicast to me and my counterpart
+            const uint16_t amask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
+            if (p.a_mn)
+              tma_load_3d_cg2_mc(sa + pair * E::BOX_BYTES, &tmap_a, &full[stage],
+                                 m0 + E::MN_ATOM * (int32_t)pair, k0, bb, amask);
+            else
+              tma_load_3d_cg2_mc(sa + pair * (A_STAGE_BYTES / 2), &tmap_a, &full[stage], k0,
+                                 m0 + (BM / 2) * (int32_t)pair, bb, amask);
+          } else if (p.a_mn) {
 #pragma unroll
             for (int j = 0; j < BM / E::MN_ATOM; ++j)
               tma_load<CG>(sa + j * E::BOX_BYTES, &tmap_a, &full[stage], m0 + E::MN_ATOM * j, k0, bb);
@@ -397,7 +421,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                                       : make_sdesc_sw128(0, 16u, 1024);
       const uint64_t b_fixed = p.b_mn ? make_sdesc_sw128(0, E::BOX_BYTES, MN_SBO, MN_LAYOUT)
                                       : make_sdesc_sw128(0, 16u, 1024);
-      const uint32_t sa0 = smem_u32(smem_a) >> 4, sb0 = smem_u32(smem_b) >> 4;
+      // the descriptor's start-address field holds bits [4,18) of the CTA-local
+      // shared address; inside a cluster the shared::cta address also carries
+      // the CTA rank in its upper bits (bit 24+), which must not spill into
+      // the LBO field (it did for the second pair of a 4-CTA cluster)
+      const uint32_t sa0 = (smem_u32(smem_a) & 0x3FFFFu) >> 4;
+      const uint32_t sb0 = (smem_u32(smem_b) & 0x3FFFFu) >> 4;
       // With a single 512-column accumulator (BN = 512) the two N = 256 halves
       // are released separately by the epilogue (tmem_empty[0] = columns
       // [0,256), tmem_empty[1] = [256,512)): the next tile's first-half MMAs
@@ -417,7 +446,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       };
       auto release = [&](int st) {
         if constexpr (CG == 1) umma_commit(&empty[st]);
-        else umma_commit_mc(&empty[st], 0x3);
+        else umma_commit_mc(&empty[st], CN == 2 ? (uint16_t)0xF : (uint16_t)0x3);
       };
       for (int64_t u = cluster_id; u < p.num_units; u += num_clusters, ++it) {
         const int nkb = unit_info(p, u).nkb;
@@ -467,7 +496,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         }
         if (elect_one()) {
           if constexpr (CG == 1) umma_commit(&tmem_full[acc]);
-          else umma_commit_mc(&tmem_full[acc], 0x3);
+          else umma_commit_mc(&tmem_full[acc], pair_mask);
         }
         __syncwarp();
       }
@@ -488,6 +517,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int64_t t = ui.t;
       int64_t b, tm, tn;
       tile_coords(p, t, b, tm, tn);
+      tn = tn * CN + pair;
       b += ui.kslice * p.batch;  // uniform split-K slices are extra output batches
       // tail-split partial: dense f32 block of the workspace for this slice
       float *wsrow = ui.slot >= 0 ? p.ws + ui.slot * (int64_t)C::TILE_M * BN +
@@ -503,7 +533,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         __syncwarp();
         if (lane == 0) {
           if constexpr (CG == 1) mbar_arrive(&tmem_empty[which]);
-          else mbar_arrive_cluster(&tmem_empty[which], 0);
+          else mbar_arrive_cluster(&tmem_empty[which], 2 * pair);   // own pair's leader
         }
       };
       if (p.debug & 4) {  // timing probe: release the accumulator without reading it
@@ -707,7 +737,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     __syncwarp();
   }
   tc_fence_before();
-  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
+  if constexpr (CL == 1) __syncthreads(); else cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
@@ -800,7 +830,7 @@ tail_fixup_kernel(const TcParams p, int tile_m, int bn) {
   }
 }
 
-template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false>
+template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false, int CN = 1>
 int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   using C = Cfg<BN, CG, (int)sizeof(OutT), IN_BYTES>;
   using E = typename C::E;
@@ -817,7 +847,8 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
     rc = make_map(&ma, d.a, dt, d.M, d.K, d.batch, d.a_stride[2], d.a_stride[0], AT, KB, IN_BYTES,
                   mn_swz);
   else
-    rc = make_map(&ma, d.a, dt, d.K, d.M, d.batch, d.a_stride[1], d.a_stride[0], KB, BM, IN_BYTES);
+    rc = make_map(&ma, d.a, dt, d.K, d.M, d.batch, d.a_stride[1], d.a_stride[0], KB, BM / CN,
+                  IN_BYTES);
   if (rc) return rc;
   if (p.b_mn)
     rc = make_map(&mb, d.b, dt, d.N, d.K, d.batch, d.b_stride[1], d.b_stride[0], AT, KB, IN_BYTES,
@@ -847,13 +878,14 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
                           : make_idesc_f16(d.in_dtype == BGX_BF16, p.a_mn, p.b_mn, C::TILE_M, C::MMA_N);
   p.stages = (d.sched.stages >= 2 && d.sched.stages <= C::STAGES) ? d.sched.stages : C::STAGES;
   p.tiles_m = (int32_t)((d.M + C::TILE_M - 1) / C::TILE_M);
-  p.tiles_n = (int32_t)((d.N + BN - 1) / BN);
+  p.tiles_n = (int32_t)(((d.N + BN - 1) / BN + CN - 1) / CN);   // schedule units along N
   p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * d.batch;
   if (p.k_splits < 1) p.k_splits = 1;
   p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
   p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
   p.num_units = p.num_tiles * p.k_splits;
-  auto kern = tc_gemm_kernel<BN, CG, OutT, IN_BYTES, RS>;
+  auto kern = tc_gemm_kernel<BN, CG, OutT, IN_BYTES, RS, CN>;
+  constexpr int CL = CG * CN;
   static thread_local int configured[64] = {0};
   static thread_local int clusters[64] = {0};
   int dev = 0;
@@ -862,12 +894,12 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
     BGX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM_BYTES));
     configured[dev & 63] = 1;
-    clusters[dev & 63] = CG == 1 ? sm_count_current() : max_clusters(kern, C::SMEM_BYTES, CG);
-    if (clusters[dev & 63] <= 0) clusters[dev & 63] = sm_count_current() / CG;
+    clusters[dev & 63] = CL == 1 ? sm_count_current() : max_clusters(kern, C::SMEM_BYTES, CL);
+    if (clusters[dev & 63] <= 0) clusters[dev & 63] = sm_count_current() / CL;
   }
   int64_t nclusters = clusters[dev & 63];
   // tail split: only the tiles of the last, partial wave are split in K
-  if (p.tail_splits > 1 && p.k_splits == 1 && C::ACC_BUFS == 2 && p.ws != nullptr) {
+  if (p.tail_splits > 1 && p.k_splits == 1 && C::ACC_BUFS == 2 && p.ws != nullptr && CN == 1) {
     const int64_t slots = nclusters;
     p.tail_start = (p.num_tiles / slots) * slots;
     const int64_t tt = p.num_tiles - p.tail_start;
@@ -885,16 +917,16 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
     p.tail_start = p.num_tiles;
   }
   if (p.num_units < nclusters) nclusters = p.num_units;
-  if (d.sched.max_ctas > 0 && nclusters * CG > d.sched.max_ctas) nclusters = d.sched.max_ctas / CG;
+  if (d.sched.max_ctas > 0 && nclusters * CL > d.sched.max_ctas) nclusters = d.sched.max_ctas / CL;
   if (nclusters < 1) nclusters = 1;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)(nclusters * CG));
+  cfg.gridDim = dim3((unsigned)(nclusters * CL));
   cfg.blockDim = dim3(NUM_THREADS);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -910,7 +942,12 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
 }
 
 template <int CG, typename OutT, int IB = 2>
-int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStream_t s) {
+int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStream_t s,
+                int cn = 1) {
+  if constexpr (CG == 2 && IB == 2) {
+    if (cn == 2 && bn == 512) return launch_tc<512, 2, OutT, 2, false, 2>(d, p, s);
+    if (cn == 2 && bn == 256) return launch_tc<256, 2, OutT, 2, false, 2>(d, p, s);
+  }
   switch (bn) {
     case 64:
       return CG == 1 ? launch_tc<64, 1, OutT, IB>(d, p, s) : launch_tc<128, CG, OutT, IB>(d, p, s);
@@ -960,8 +997,9 @@ void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
     const double cost = (double)split_waves * (double)(128 * c.bn) / c.eff / (double)sp *
                         (sp > 1 ? 1.1 : 1.0);
     // single 512-column accumulator: its drain is amortised only over long K
-    // and many waves (4096^3 measured faster with 256-wide tiles)
-    if (c.bn == 512 && (d.N < 1024 || d.K < 8192 || waves < 8)) continue;
+    // and several waves (4096^3 measured faster with 256-wide tiles; 8192^3,
+    // 7 waves, 5 % faster with 512: profiles/r01_tile512_8192.txt)
+    if (c.bn == 512 && (d.N < 1024 || d.K < 8192 || waves < 4)) continue;
     if (best < 0 || cost < best * 0.97) {
       best = cost;
       cg = c.cg;
@@ -1030,14 +1068,17 @@ int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s, int
   // columns) L2-resident while A streams (-8); otherwise M-groups.
   p.raster = d.sched.raster != 0 ? d.sched.raster : (bn == 512 ? -8 : (cg == 2 ? 8 : 16));
   p.debug = d.sched.reserved[0];
+  // two CTA pairs per cluster sharing A by multicast (schedule reserved[1]
+  // = cluster_n; not with the tail split, whose workspace slots are per unit)
+  const int cn = (cg == 2 && d.sched.reserved[1] == 2 && tail_splits <= 1) ? 2 : 1;
   if (d.in_dtype == BGX_F32)  // tf32 tensor cores (opt-in BGX_MODE_TF32)
     return cg == 2 ? dispatch_bn<2, float, 4>(d, bn, p, s) : dispatch_bn<1, float, 4>(d, bn, p, s);
   if (d.out_dtype == BGX_F32)
-    return cg == 2 ? dispatch_bn<2, float>(d, bn, p, s) : dispatch_bn<1, float>(d, bn, p, s);
+    return cg == 2 ? dispatch_bn<2, float>(d, bn, p, s, cn) : dispatch_bn<1, float>(d, bn, p, s);
   if (d.out_dtype == BGX_BF16)
-    return cg == 2 ? dispatch_bn<2, __nv_bfloat16>(d, bn, p, s)
+    return cg == 2 ? dispatch_bn<2, __nv_bfloat16>(d, bn, p, s, cn)
                    : dispatch_bn<1, __nv_bfloat16>(d, bn, p, s);
-  return cg == 2 ? dispatch_bn<2, __half>(d, bn, p, s) : dispatch_bn<1, __half>(d, bn, p, s);
+  return cg == 2 ? dispatch_bn<2, __half>(d, bn, p, s, cn) : dispatch_bn<1, __half>(d, bn, p, s);
 }
 
 // out[b,m,n] = (c0) + sum_s ws[s][b][m][n], summed in increasing s (deterministic).

@@ -162,6 +162,8 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
             if k == "reserved":
                 for i, x in enumerate(v):
                     d.sched.reserved[i] = int(x)
+            elif k == "cluster_n":
+                d.sched.reserved[1] = int(v)
             else:
                 setattr(d.sched, k, int(v))
     kind = lib.bgx_contract_kernel(d)

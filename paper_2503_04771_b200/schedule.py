@@ -21,7 +21,7 @@ from __future__ import annotations
 
 from dataclasses import asdict, dataclass
 
-_KEYS = ("tile_n", "stages", "cta_group", "raster", "splits", "max_ctas")
+_KEYS = ("tile_n", "stages", "cta_group", "raster", "splits", "max_ctas", "cluster_n")
 
 
 @dataclass(frozen=True)
@@ -32,6 +32,7 @@ class Schedule:
     raster: int = 0       # >0: groups of M tiles; <0: groups of N tiles
     splits: int = 0       # split-K slices (>1), or tail split of the last wave (<-1)
     max_ctas: int = 0     # cap on persistent CTAs
+    cluster_n: int = 0    # 2: two CTA pairs per cluster along N share A by TMA multicast
 
     def to_dict(self) -> dict:
         return {k: v for k, v in asdict(self).items() if v}

@@ -303,3 +303,35 @@ def test_tail_split_matches_unsplit(dev, M, N, K):
     assert oracle.rel_frobenius(np32(tail)[rows], want) <= 1e-5
     bf = contract("(i,k),(k,j)->(i,j)", a, b, schedule={"splits": -3})
     assert oracle.rel_frobenius(np32(bf), np32(plain) - np32(c0)) <= BF16_TOL
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(512, 1024, 512, 256), (768, 1280, 640, 256),
+                                      (1024, 2560, 8192, 512), (256, 768, 192, 256)])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, True), (True, False), (True, True), (False, False)])
+def test_cluster_n2_a_multicast_bit_equal(dev, M, N, K, bn, a_mn, b_mn):
+    """Two CTA pairs per cluster sharing A by TMA multicast (schedule
+    cluster_n=2) compute exactly what one pair computes (same MMA order):
+    bit-equal, any operand majorness, odd tile counts along N (the second
+    pair's tile falls outside N), f32 out and c0."""
+    g = torch.Generator(device=dev).manual_seed(M + N + K)
+    a = torch.randn(M, K, device=dev, generator=g).bfloat16()
+    b = torch.randn(K, N, device=dev, generator=g).bfloat16()
+    a_in = a.t().contiguous().t() if a_mn else a
+    b_in = b if b_mn else b.t().contiguous().t()
+    for out_dtype, c0 in ((torch.bfloat16, None), (torch.float32, torch.randn(M, N, device=dev))):
+        base = contract("(i,k),(k,j)->(i,j)", a_in, b_in, out_dtype=out_dtype, c0=c0,
+                        schedule={"tile_n": bn, "cta_group": 2, "no_splitk": 1})
+        y = contract("(i,k),(k,j)->(i,j)", a_in, b_in, out_dtype=out_dtype, c0=c0,
+                     schedule={"tile_n": bn, "cta_group": 2, "cluster_n": 2, "no_splitk": 1})
+        assert torch.equal(y, base)
+    want = a.double() @ b.double()
+    assert float((base.double() - want - c0.double()).norm() / want.norm()) < 1e-5
+
+
+def test_cluster_n2_batched(dev):
+    a = torch.randn(6, 384, 512, device=dev).half()
+    b = torch.randn(6, 512, 640, device=dev).half()
+    sc = {"tile_n": 256, "cta_group": 2}
+    base = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, schedule=sc)
+    y = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, schedule=dict(sc, cluster_n=2))
+    assert torch.equal(y, base)
