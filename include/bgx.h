@@ -167,8 +167,9 @@ BGX_API int bgx_contract_tile(const bgx_contract_desc *d, int32_t *cta_group, in
  * floats), then one reduction kernel sums the slices in order, adds c0 and
  * casts.  splits < -1 selects the TAIL split instead (stream-K style): full
  * waves of tiles run unsplit and only the tiles of the last, partial wave are
- * split into -splits K slices (f32 partials in `workspace`, then a fix-up
- * kernel).  bgx_contract_splitk_plan returns the split count the library
+ * split into -splits K slices (f32 partials in `workspace`; the last slice of
+ * each tile to finish sums the slices in slice order inside the same kernel —
+ * deterministic — and writes the output).  bgx_contract_splitk_plan returns the split count the library
  * would use (1 = neither is worth it) and the workspace size in bytes.     */
 BGX_API int bgx_contract_splitk_plan(const bgx_contract_desc *d, int32_t *splits,
                                      int64_t *workspace_bytes);

@@ -59,11 +59,16 @@ struct TcParams {
   int32_t k_splits, kb_per_split;  // split-K: unit u -> tile u % num_tiles, K slice u / num_tiles
   int64_t num_units;
   // tail split (stream-K style): tiles >= tail_start are split into
-  // tail_splits K slices whose f32 partials go to `ws` (one dense
-  // TILE_M x BN block per slice) and are reduced by tail_fixup_kernel
+  // tail_splits K slices; slices 0..S-2 store f32 partials to `ws` (one
+  // TILE_M x BN block per slice) and count themselves in tail_counters; the
+  // last slice (the finisher) waits for that count — every CTA of the
+  // persistent grid is resident and every tile's other slices come earlier
+  // in each CTA's unit order, so the wait cannot deadlock — and adds the
+  // partials, in slice order, to its own accumulator before storing
   int64_t tail_start;
   int32_t tail_splits, kb_per_tail;
   float *ws;
+  uint32_t *tail_counters;
   int64_t ws_bytes;
   uint32_t idesc;
   int32_t a_mn, b_mn;            // 1 = MN-major operand
@@ -519,10 +524,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       tile_coords(p, t, b, tm, tn);
       tn = tn * CN + pair;
       b += ui.kslice * p.batch;  // uniform split-K slices are extra output batches
-      // tail-split partial: dense f32 block of the workspace for this slice
-      float *wsrow = ui.slot >= 0 ? p.ws + ui.slot * (int64_t)C::TILE_M * BN +
-                                        (int64_t)(rank * BM + quad * 32 + lane) * BN
-                                  : nullptr;
+      // tail-split partial: f32 block of the workspace for this slice, stored
+      // column-major inside each 32-column chunk ([c][j][row]) so that a
+      // warp's 32 rows of one column are one coalesced 128-byte line
+      const int row_in_tile = (int)(rank * BM + quad * 32 + lane);
+      const bool tail = ui.slot >= 0;
+      const int64_t tt = p.num_tiles - p.tail_start;
+      const bool finisher = tail && ui.slot / tt == p.tail_splits - 1;
+      float *wsrow = tail && !finisher
+                         ? p.ws + ui.slot * (int64_t)C::TILE_M * BN + row_in_tile : nullptr;
+      uint32_t *tcount = tail ? p.tail_counters + (t - p.tail_start) * CG + rank : nullptr;
       const int acc = it % C::ACC_BUFS;
       const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
       mbar_wait(&tmem_full[acc], acc_phase);
@@ -692,6 +703,61 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           continue;
         }
       }
+      // one 32-column chunk of this thread's output row: TMA store through the
+      // warp's swizzled staging buffer, or direct stores
+      auto store_out = [&](const float *v, int64_t n, int64_t valid) {
+        if (p.tma_store) {
+          uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
+          ++chunk;
+          if (lane == 0) bulk_wait_read<1>();   // the buffer used two chunks ago is free
+          __syncwarp();
+          stage_row32<OutT>(buf, lane, v);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmap_o, buf, (int32_t)n, (int32_t)m_warp, (int32_t)b);
+            bulk_commit();
+          }
+        } else if (row_ok) {
+          Store<OutT>::row32(orow + n, v, valid >= 32, valid);
+        }
+      };
+      if (finisher) {   // wait until the tile's other K slices stored their partials
+        if (threadIdx.x == 128)
+          while (ld_acquire_gpu(tcount) < (uint32_t)(p.tail_splits - 1)) __nanosleep(64);
+        named_bar_sync(1, 32 * EPI_WARPS);
+        __threadfence();
+      }
+      if (finisher) {
+        // (((0 + p_0) + p_1) + ...) + own slice: fixed order whatever the timing
+        const float *part0 = p.ws + (t - p.tail_start) * (int64_t)C::TILE_M * BN + row_in_tile;
+#pragma unroll 1
+        for (int c = g; c < NCHUNK; c += 2) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + c * 32, r);
+          tmem_ld_wait();
+          const int64_t n = tn * BN + c * 32;
+          if (n >= p.N) continue;
+          const int64_t valid = p.N - n;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          for (int sl = 0; sl < p.tail_splits - 1; ++sl) {
+            const float *wc = part0 + sl * tt * (int64_t)C::TILE_M * BN +
+                              (int64_t)(c * 32) * C::TILE_M;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], __ldcg(wc + j * C::TILE_M));
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], __uint_as_float(r[j]));
+          if (crow && row_ok)
+            for (int j = 0; j < 32; ++j)
+              if (j < valid) v[j] = __fadd_rn(v[j], Conv<OutT>::to_f(crow[n + j]));
+          store_out(v, n, valid);
+        }
+        arrive_empty(SPLIT_RELEASE ? 1 : acc);
+        continue;
+      }
       uint32_t rbuf[2][32];
       tmem_ld_32x32b_x32(taddr + g * 32, rbuf[0]);
 #pragma unroll 2
@@ -712,25 +778,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
             if (j < valid) v[j] = __fadd_rn(v[j], Conv<OutT>::to_f(crow[n + j]));
         }
         if (wsrow != nullptr) {
-          Store<float>::row32(wsrow + c * 32, v, true, 32);
-        } else if (p.tma_store) {
-          uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
-          ++chunk;
-          if (lane == 0) bulk_wait_read<1>();   // the buffer used two chunks ago is free
-          __syncwarp();
-          stage_row32<OutT>(buf, lane, v);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&tmap_o, buf, (int32_t)n, (int32_t)m_warp, (int32_t)b);
-            bulk_commit();
-          }
-        } else if (row_ok) {
-          Store<OutT>::row32(orow + n, v, valid >= 32, valid);
+          float *wc = wsrow + (int64_t)(c * 32) * C::TILE_M;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) __stcg(wc + j * C::TILE_M, v[j]);
+        } else {
+          store_out(v, n, valid);
         }
       }
       tmem_ld_wait();
       arrive_empty(SPLIT_RELEASE ? 1 : acc);
+      if (wsrow != nullptr) {   // publish this slice's partial to the finisher
+        __threadfence();
+        named_bar_sync(1, 32 * EPI_WARPS);
+        if (threadIdx.x == 128) atomicAdd(tcount, 1u);
+      }
       }  // !RS
     }
     if (lane == 0) bulk_wait_all();
@@ -805,29 +866,6 @@ int max_clusters(K kern, int smem, int cg) {
     return 0;
   }
   return n;
-}
-
-// out = c0 + sum over K slices of the tail tiles' f32 partials (slices in order)
-template <typename OutT>
-__global__ void __launch_bounds__(256)
-tail_fixup_kernel(const TcParams p, int tile_m, int bn) {
-  const int64_t tt = p.num_tiles - p.tail_start;
-  const int64_t per_tile = (int64_t)tile_m * bn;
-  const int64_t total = tt * per_tile;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ti = i / per_tile, e = i % per_tile;
-    const int64_t r = e / bn, c = e % bn;
-    int64_t b, tm, tn;
-    tile_coords(p, p.tail_start + ti, b, tm, tn);
-    const int64_t m = tm * tile_m + r, n = tn * bn + c;
-    if (m >= p.M || n >= p.N) continue;
-    float v = 0.f;
-    for (int sl = 0; sl < p.tail_splits; ++sl) v = __fadd_rn(v, p.ws[(sl * tt + ti) * per_tile + e]);
-    if (p.c0)
-      v = __fadd_rn(v, Conv<OutT>::to_f(static_cast<const OutT *>(p.c0)[b * p.sc[0] + m * p.sc[1] + n * p.sc[2]]));
-    static_cast<OutT *>(p.out)[b * p.so[0] + m * p.so[1] + n * p.so[2]] = Conv<OutT>::from_f(v);
-  }
 }
 
 template <int BN, int CG, typename OutT, int IN_BYTES, bool RS = false, int CN = 1>
@@ -905,12 +943,15 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
     const int64_t tt = p.num_tiles - p.tail_start;
     p.kb_per_tail = (p.k_blocks + p.tail_splits - 1) / p.tail_splits;
     p.tail_splits = (p.k_blocks + p.kb_per_tail - 1) / p.kb_per_tail;
-    const int64_t need = tt * p.tail_splits * (int64_t)C::TILE_M * BN * 4;
+    const int64_t part = (tt * p.tail_splits * (int64_t)C::TILE_M * BN * 4 + 255) / 256 * 256;
+    const int64_t need = part + tt * CG * 4;
     if (tt == 0 || p.tail_splits < 2 || need > p.ws_bytes) {
       p.tail_splits = 1;
       p.tail_start = p.num_tiles;
     } else {
       p.num_units = p.tail_start + tt * p.tail_splits;
+      p.tail_counters = reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(p.ws) + part);
+      BGX_CUDA_TRY(cudaMemsetAsync(p.tail_counters, 0, tt * CG * 4, s));
     }
   } else {
     p.tail_splits = 1;
@@ -932,13 +973,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   BGX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, p));
-  int rc2 = check_launch("tc_gemm_kernel");
-  if (rc2 || p.tail_splits <= 1) return rc2;
-  const int64_t total = (p.num_tiles - p.tail_start) * (int64_t)C::TILE_M * BN;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > (int64_t)sm_count_current() * 8) blocks = (int64_t)sm_count_current() * 8;
-  tail_fixup_kernel<OutT><<<(unsigned)blocks, 256, 0, s>>>(p, C::TILE_M, BN);
-  return check_launch("tail_fixup_kernel");
+  return check_launch("tc_gemm_kernel");
 }
 
 template <int CG, typename OutT, int IB = 2>
@@ -1115,18 +1150,17 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
   const int64_t k_blocks = (d.K + BKe - 1) / BKe;
   const int64_t sp = uniform_splits(tiles, slots, k_blocks);
   if (sp == 1) {
-    // tail split: when the last wave is less than 3/4 full, split only its
-    // tiles in K (reported as a negative split count)
-    // (measured on B200: at K = 4096 the partial-tile stores + fix-up cost
-    // more than the saved half wave — 1091 vs 1430 TFLOP/s on 4096^3 — so the
-    // automatic plan only uses it for long K; schedule {"splits": -S} forces it)
+    // tail split: when the last wave is at most half full, split only its
+    // tiles in two K halves (reported as a negative split count); the second
+    // half finishes the tile inside the kernel.  Measured on B200
+    // (profiles/r01_tail_split.txt): +2-18 % for K >= 8192, break-even at
+    // 4096^3 (the partial exchange costs about the half wave it saves),
+    // slower for K = 2048; 3- and 4-way splits never beat 2.
     const int64_t tail = tiles % slots;
-    if (bn > 256 || tiles < slots || tail == 0 || tail * 4 > slots * 3 || k_blocks < 512) return;
-    int64_t ts = slots / tail;
-    if (ts > 4) ts = 4;
-    if (ts < 2) return;
+    if (bn > 256 || tiles < slots || tail == 0 || tail * 2 > slots || k_blocks < 128) return;
+    const int64_t ts = 2;
     *splits = -(int)ts;
-    *ws_bytes = (slots - 1) * ts * (int64_t)(128 * cg) * bn * 4;
+    *ws_bytes = (slots - 1) * ts * (int64_t)(128 * cg) * bn * 4 + 256 + slots * cg * 4;
     return;
   }
   *splits = (int)sp;
