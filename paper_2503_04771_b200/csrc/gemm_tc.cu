@@ -657,7 +657,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       OutT *orow = static_cast<OutT *>(p.out) + b * p.so[0] + m * p.so[1];
       const OutT *crow = p.c0 ? static_cast<const OutT *>(p.c0) + b * p.sc[0] + m * p.sc[1] : nullptr;
       if constexpr (SPLIT_RELEASE && sizeof(OutT) == 2) {
-        if (p.tma_store && crow == nullptr && !(p.debug & 1)) {
+        if (p.tma_store && crow == nullptr && !(p.debug & 1) && !tail) {
           // Two-phase drain: read this warp's chunks of each accumulator half
           // into packed 16-bit registers, release that half of TMEM to the MMA
           // warp, and only then stage + TMA-store — the stores (and their
@@ -736,6 +736,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + c * 32, r);
           tmem_ld_wait();
+          if (SPLIT_RELEASE && c >= NCHUNK / 2 && c - 2 < NCHUNK / 2)
+            arrive_empty(0);  // every chunk of columns [0, BN/2) has been read
           const int64_t n = tn * BN + c * 32;
           if (n >= p.N) continue;
           const int64_t valid = p.N - n;
@@ -937,7 +939,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   }
   int64_t nclusters = clusters[dev & 63];
   // tail split: only the tiles of the last, partial wave are split in K
-  if (p.tail_splits > 1 && p.k_splits == 1 && C::ACC_BUFS == 2 && p.ws != nullptr && CN == 1) {
+  if (p.tail_splits > 1 && p.k_splits == 1 && p.ws != nullptr && CN == 1) {
     const int64_t slots = nclusters;
     p.tail_start = (p.num_tiles / slots) * slots;
     const int64_t tt = p.num_tiles - p.tail_start;
@@ -1029,8 +1031,12 @@ void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
     const int64_t sp = uniform_splits(tiles, slots, k_blocks);
     const int64_t waves = (tiles + slots - 1) / slots;
     const int64_t split_waves = (tiles * sp + slots - 1) / slots;
-    const double cost = (double)split_waves * (double)(128 * c.bn) / c.eff / (double)sp *
-                        (sp > 1 ? 1.1 : 1.0);
+    double eff_waves = (double)split_waves / (double)sp * (sp > 1 ? 1.1 : 1.0);
+    // a last wave at most half full gets the 2-way tail split (tc_splitk_plan)
+    const int64_t tail = tiles % slots;
+    if (sp == 1 && tiles >= slots && tail > 0 && tail * 2 <= slots && k_blocks >= 128)
+      eff_waves = (double)(tiles / slots) + 0.55;
+    const double cost = eff_waves * (double)(128 * c.bn) / c.eff;
     // single 512-column accumulator: its drain is amortised only over long K
     // and several waves (4096^3 measured faster with 256-wide tiles; 8192^3,
     // 7 waves, 5 % faster with 512: profiles/r01_tile512_8192.txt)
@@ -1157,7 +1163,7 @@ void tc_splitk_plan(const bgx_contract_desc &d, int *splits, int64_t *ws_bytes) 
     // 4096^3 (the partial exchange costs about the half wave it saves),
     // slower for K = 2048; 3- and 4-way splits never beat 2.
     const int64_t tail = tiles % slots;
-    if (bn > 256 || tiles < slots || tail == 0 || tail * 2 > slots || k_blocks < 128) return;
+    if (tiles < slots || tail == 0 || tail * 2 > slots || k_blocks < 128) return;
     const int64_t ts = 2;
     *splits = -(int)ts;
     *ws_bytes = (slots - 1) * ts * (int64_t)(128 * cg) * bn * 4 + 256 + slots * cg * 4;

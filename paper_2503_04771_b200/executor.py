@@ -175,7 +175,7 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
         if schedule and schedule.get("splits"):
             splits.value = int(schedule["splits"])
             if splits.value < -1:   # forced tail split: upper-bound workspace
-                ws_bytes.value = lib.bgx_sm_count() * (-splits.value * 256 * 256 * 4 + 8) + 256
+                ws_bytes.value = lib.bgx_sm_count() * (-splits.value * 256 * 512 * 4 + 8) + 256
             else:
                 ws_bytes.value = splits.value * batch * M * N * 4
     if schedule and kind == _lib.KERNEL_TC:

@@ -284,25 +284,29 @@ def test_tf32_c1_config_and_splitk(dev):
     assert oracle.rel_frobenius(np32(out), ref) <= TF32_TOL
 
 
-@pytest.mark.parametrize("M,N,K", [(2304, 2560, 2048), (4096, 4096, 4096)])
-def test_tail_split_matches_unsplit(dev, M, N, K):
+@pytest.mark.parametrize("M,N,K,bn", [(2304, 2560, 2048, 0), (4096, 4096, 4096, 0),
+                                      (4096, 4608, 1024, 512), (2816, 3072, 8192, 512)])
+def test_tail_split_matches_unsplit(dev, M, N, K, bn):
     """Stream-K-style tail split: only the last partial wave's tiles are split
     in K; results match the unsplit kernel to f32 summation-order noise and
     the oracle on sampled rows."""
     a, b = rnd((M, K), 81, dev, torch.bfloat16), rnd((K, N), 82, dev, torch.bfloat16)
     c0 = rnd((M, N), 83, dev, torch.float32)
+    tile = {"tile_n": bn, "cta_group": 2} if bn else {}
     executor.reset_launch_log()
     tail = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, out_dtype=torch.float32,
-                    schedule={"splits": -2})
+                    schedule=dict(tile, splits=-2))
     assert executor.launch_log() == ["tcgen05-tailsplit"], executor.launch_log()
     plain = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, out_dtype=torch.float32,
-                     schedule={"no_splitk": 1})
+                     schedule=dict(tile, no_splitk=1))
     assert oracle.rel_frobenius(np32(tail), np32(plain)) <= 1e-5
     rows = np.r_[0:4, M - 260:M - 250, M - 4:M]
     want = oracle.gemm_kseq(np.ascontiguousarray(np32(a)[rows]), np32(b), np32(c0)[rows])
     assert oracle.rel_frobenius(np32(tail)[rows], want) <= 1e-5
-    bf = contract("(i,k),(k,j)->(i,j)", a, b, schedule={"splits": -3})
+    bf = contract("(i,k),(k,j)->(i,j)", a, b, schedule=dict(tile, splits=-3))
     assert oracle.rel_frobenius(np32(bf), np32(plain) - np32(c0)) <= BF16_TOL
+    again = contract("(i,k),(k,j)->(i,j)", a, b, schedule=dict(tile, splits=-3))
+    assert torch.equal(bf, again)   # deterministic whatever the arrival order
 
 
 @pytest.mark.parametrize("M,N,K,bn", [(512, 1024, 512, 256), (768, 1280, 640, 256),
