@@ -11,6 +11,8 @@ widened to f32.
 
 from __future__ import annotations
 
+import threading
+
 import torch
 
 from . import executor
@@ -117,24 +119,22 @@ def contract_host(spec, *host_operands: torch.Tensor, out: torch.Tensor | None =
     dt = kw.get("out_dtype") or host_operands[0].dtype
     if out is None:
         out = torch.empty(out_shape, dtype=dt, pin_memory=True)
-    comp = torch.cuda.current_stream(device)
-    h2d = torch.cuda.Stream(device)
-    d2h = torch.cuda.Stream(device)
     a = host_operands[0]
+    nbuf = 2
+    st = _staging(device, chunk_rows, nbuf, a, host_operands[1:], out_shape, dt,
+                  c0.dtype if c0 is not None else None)
+    comp = torch.cuda.current_stream(device)
+    h2d, d2h = st["h2d"], st["d2h"]
+    h2d.wait_stream(comp)          # staging buffers: the previous call's work is done
+    d2h.wait_stream(comp)
     with torch.cuda.stream(h2d):
-        others = [t.to(device, non_blocking=True) for t in host_operands[1:]]
-    for t in others:
-        t.record_stream(comp)
+        others = st["others"]
+        for dst, src in zip(others, host_operands[1:]):
+            dst.copy_(src, non_blocking=True)
     others_ready = torch.cuda.Event()
     others_ready.record(h2d)
     n_chunks = (rows + chunk_rows - 1) // chunk_rows
-    nbuf = 2
-    a_buf = [torch.empty((chunk_rows, *a.shape[1:]), dtype=a.dtype, device=device)
-             for _ in range(nbuf)]
-    o_buf = [torch.empty((chunk_rows, *out_shape[1:]), dtype=dt, device=device)
-             for _ in range(nbuf)]
-    c_buf = ([torch.empty((chunk_rows, *out_shape[1:]), dtype=c0.dtype, device=device)
-              for _ in range(nbuf)] if c0 is not None else None)
+    a_buf, o_buf, c_buf = st["a"], st["o"], st["c"]
     ev_h2d = [torch.cuda.Event() for _ in range(n_chunks)]
     ev_comp = [torch.cuda.Event() for _ in range(n_chunks)]
     ev_d2h = [torch.cuda.Event() for _ in range(n_chunks)]
@@ -161,6 +161,37 @@ def contract_host(spec, *host_operands: torch.Tensor, out: torch.Tensor | None =
             d2h.wait_event(ev_comp[i])
             out[r0:r1].copy_(o_buf[slot][:n], non_blocking=True)
             ev_d2h[i].record(d2h)
-    d2h.synchronize()
+    comp.wait_stream(d2h)
+    comp.wait_stream(h2d)
     comp.synchronize()
     return out
+
+
+_staging_cache = threading.local()
+
+
+def _staging(device, chunk_rows, nbuf, a, others, out_shape, dt, c0_dtype):
+    """Device staging buffers + copy streams for contract_host, kept per
+    thread and reused across calls with the same shapes (no allocator churn
+    on the hot e2e path: per-call allocations with cross-stream frees made
+    the caching allocator fall back to fresh cudaMallocs)."""
+    key = (str(device), chunk_rows, nbuf, tuple(a.shape[1:]), a.dtype,
+           tuple((tuple(t.shape), t.dtype) for t in others), tuple(out_shape[1:]), dt, c0_dtype)
+    cache = getattr(_staging_cache, "d", None)
+    if cache is None:
+        cache = _staging_cache.d = {}
+    st = cache.get(key)
+    if st is None:
+        cache.clear()            # one resident set per thread: drop stale shapes
+        st = {
+            "h2d": torch.cuda.Stream(device), "d2h": torch.cuda.Stream(device),
+            "others": [torch.empty(t.shape, dtype=t.dtype, device=device) for t in others],
+            "a": [torch.empty((chunk_rows, *a.shape[1:]), dtype=a.dtype, device=device)
+                  for _ in range(nbuf)],
+            "o": [torch.empty((chunk_rows, *out_shape[1:]), dtype=dt, device=device)
+                  for _ in range(nbuf)],
+            "c": ([torch.empty((chunk_rows, *out_shape[1:]), dtype=c0_dtype, device=device)
+                   for _ in range(nbuf)] if c0_dtype is not None else None),
+        }
+        cache[key] = st
+    return st
