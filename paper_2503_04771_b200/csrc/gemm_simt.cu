@@ -53,13 +53,21 @@ struct Params {
 
 constexpr int BK = 16;
 
+// BM x BN tile, TM x TN outputs per thread, K staged through shared memory
+// in KT-deep tiles; the next tile's elements are loaded into registers while
+// the current one is multiplied (one round trip of global-load latency per
+// tile is otherwise exposed — it dominated small, latency-bound problems).
+// Each output accumulates its products in increasing k from c0, so EXACT
+// mode stays bit-identical to the reference.
 template <typename In, typename Out, typename Acc, bool FUSED, int BM, int BN, int TM = 4,
-          int TN = 4>
+          int TN = 4, int KT = BK>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 simt_gemm_kernel(const Params p) {
   constexpr int NT = (BM / TM) * (BN / TN);
-  __shared__ Acc As[BK][BM + 1];
-  __shared__ Acc Bs[BK][BN + 1];
+  constexpr int LA = BM * KT / NT, LB = BN * KT / NT;   // elements per thread per tile
+  static_assert(LA * NT == BM * KT && LB * NT == BN * KT, "tile / thread mismatch");
+  __shared__ Acc As[KT][BM + 1];
+  __shared__ Acc Bs[KT][BN + 1];
   const int tid = threadIdx.x;
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
   int64_t t = blockIdx.x;
@@ -86,21 +94,47 @@ simt_gemm_kernel(const Params p) {
   // load mapping: run threads along whichever global dim has unit stride
   const bool a_k_inner = p.sa[2] == 1;
   const bool b_n_inner = p.sb[2] == 1 || p.sb[1] != 1;
-  for (int64_t k0 = 0; k0 < p.K; k0 += BK) {
-    for (int e = tid; e < BM * BK; e += NT) {
+  Acc ra[LA], rb[LB];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int l = 0; l < LA; ++l) {
+      const int e = tid + l * NT;
       int mm, kk;
-      if (a_k_inner) { kk = e % BK; mm = e / BK; } else { mm = e % BM; kk = e / BM; }
+      if (a_k_inner) { kk = e % KT; mm = e / KT; } else { mm = e % BM; kk = e / BM; }
       const int64_t m = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (m < p.M && k < p.K) ? to_acc<In, Acc>(A[m * p.sa[1] + k * p.sa[2]]) : (Acc)0;
+      ra[l] = (m < p.M && k < p.K) ? to_acc<In, Acc>(A[m * p.sa[1] + k * p.sa[2]]) : (Acc)0;
     }
-    for (int e = tid; e < BN * BK; e += NT) {
+#pragma unroll
+    for (int l = 0; l < LB; ++l) {
+      const int e = tid + l * NT;
       int nn, kk;
-      if (b_n_inner) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+      if (b_n_inner) { nn = e % BN; kk = e / BN; } else { kk = e % KT; nn = e / KT; }
       const int64_t n = n0 + nn, k = k0 + kk;
-      Bs[kk][nn] = (n < p.N && k < p.K) ? to_acc<In, Acc>(B[k * p.sb[1] + n * p.sb[2]]) : (Acc)0;
+      rb[l] = (n < p.N && k < p.K) ? to_acc<In, Acc>(B[k * p.sb[1] + n * p.sb[2]]) : (Acc)0;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int l = 0; l < LA; ++l) {
+      const int e = tid + l * NT;
+      int mm, kk;
+      if (a_k_inner) { kk = e % KT; mm = e / KT; } else { mm = e % BM; kk = e / BM; }
+      As[kk][mm] = ra[l];
+    }
+#pragma unroll
+    for (int l = 0; l < LB; ++l) {
+      const int e = tid + l * NT;
+      int nn, kk;
+      if (b_n_inner) { nn = e % BN; kk = e / BN; } else { kk = e % KT; nn = e / KT; }
+      Bs[kk][nn] = rb[l];
+    }
+  };
+  if (p.K > 0) load(0);
+  for (int64_t k0 = 0; k0 < p.K; k0 += KT) {
+    stash();
     __syncthreads();
-    const int kmax = (p.K - k0) < BK ? (int)(p.K - k0) : BK;
+    if (k0 + KT < p.K) load(k0 + KT);    // in flight while this tile is multiplied
+    const int kmax = (p.K - k0) < KT ? (int)(p.K - k0) : KT;
     for (int kk = 0; kk < kmax; ++kk) {
       Acc av[TM], bv[TN];
 #pragma unroll
@@ -292,7 +326,7 @@ int launch(const bgx_contract_desc &d, cudaStream_t s) {
     // k-sequential chain is the floor, so maximise the number of chains)
     p.tiles_m = (d.M + 15) / 16; p.tiles_n = (d.N + 15) / 16;
     int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
-    simt_gemm_kernel<In, Out, Acc, FUSED, 16, 16, 1, 1><<<(unsigned)blocks, 256, 0, s>>>(p);
+    simt_gemm_kernel<In, Out, Acc, FUSED, 16, 16, 1, 1, 64><<<(unsigned)blocks, 256, 0, s>>>(p);
   } else if (small) {
     p.tiles_m = (d.M + 31) / 32; p.tiles_n = (d.N + 31) / 32;
     int64_t blocks = p.tiles_m * p.tiles_n * d.batch;

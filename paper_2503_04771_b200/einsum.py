@@ -23,6 +23,7 @@ tensor-core input types.
 
 from __future__ import annotations
 
+import functools
 import itertools
 from dataclasses import dataclass, field
 
@@ -154,7 +155,15 @@ def _index_tuple(body: str, what: str) -> tuple:
 
 def parse_einsum(text: str) -> EinsumSpec:
     """Parse ``(i,k),(k,j)->(i,j)``; axis order = output indices, then the
-    input-only indices in first-appearance order (einsum.py:57-82)."""
+    input-only indices in first-appearance order (einsum.py:57-82).
+    Results are memoised per text (EinsumSpec is immutable; errors are not
+    cached, so every bad spec raises again)."""
+    if isinstance(text, str):
+        return _parse_cached(text)
+    return _parse(text)
+
+
+def _parse(text: str) -> EinsumSpec:
     if "->" not in text:
         raise EinsumError("einsum spec needs '->'")
     lhs, rhs = text.split("->", 1)
@@ -169,6 +178,9 @@ def parse_einsum(text: str) -> EinsumSpec:
             raise EinsumError(f"output index '{n}' does not appear in any input")
     axes = output + tuple(n for n in first_seen if n not in output)
     return EinsumSpec(inputs, output, axes)
+
+
+_parse_cached = functools.lru_cache(maxsize=4096)(_parse)
 
 
 def derive_maps(spec: EinsumSpec):

@@ -12,6 +12,7 @@ never mutated, interp.py:399) — or the permuted input for a passthrough body.
 
 from __future__ import annotations
 
+import contextlib
 import threading
 
 import torch
@@ -61,6 +62,14 @@ def _stream_ptr(t: torch.Tensor):
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
+def _on_device(dev):
+    """Context switching torch's current device to ``dev`` only when needed
+    (entering ``torch.cuda.device`` costs microseconds on every call)."""
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(dev)
+
+
 def _check_device(tensors):
     dev = None
     for t in tensors:
@@ -89,7 +98,7 @@ def permute(x: torch.Tensor, out: torch.Tensor, perm) -> torch.Tensor:
             desc.shape[d] = t.shape[d]
             desc.stride[d] = t.stride(d)
     p = (_lib._i32 * max(1, len(perm)))(*perm)
-    with torch.cuda.device(x.device):
+    with _on_device(x.device):
         _lib.check(lib.bgx_permute(ti, to, p, _stream_ptr(x)), "bgx_permute")
     _log("permute")
     return out
@@ -122,7 +131,7 @@ def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
                      list(range(c0.dim())))
     d.c0 = c0.data_ptr()
     d.out = out.data_ptr()
-    with torch.cuda.device(out.device):
+    with _on_device(out.device):
         _lib.check(lib.bgx_generic(d, _stream_ptr(out)), "bgx_generic")
     _log("generic")
     return out
@@ -182,7 +191,7 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
         cg, bn = _lib._i32(0), _lib._i32(0)
         _lib.check(lib.bgx_contract_tile(d, cg, bn), "bgx_contract_tile")
         tile_log().append((cg.value, bn.value, splits.value))
-    with torch.cuda.device(out.device):
+    with _on_device(out.device):
         if splits.value > 1 or splits.value < -1:
             ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=out.device)
             _lib.check(lib.bgx_contract_splitk(d, splits.value, ws.data_ptr(), ws_bytes.value,

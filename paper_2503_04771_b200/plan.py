@@ -25,6 +25,8 @@ Everything here is host logic over integers — unit-tested on the CPU
 
 from __future__ import annotations
 
+import functools
+
 from dataclasses import dataclass, field
 
 from .einsum import EinsumSpec
@@ -155,7 +157,26 @@ def plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "
                  out_strides=None, chain_order: str = "left"):
     """Plan one generic op.  ``shapes``/``strides``: per operand (inputs then
     output), element strides.  ``dtype``: 'f32'|'f64'|'bf16'|'f16'.
-    ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt'."""
+    ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt'.  Plans are pure
+    functions of these arguments and are memoised (callers treat them as
+    read-only); invalid shapes raise every time."""
+    key = (spec, tuple(tuple(s) for s in shapes), tuple(tuple(s) for s in strides), dtype, mode,
+           None if out_strides is None else tuple(out_strides), chain_order)
+    try:
+        return _plan_cached(*key)
+    except TypeError:          # unhashable argument: plan without the cache
+        return _plan_generic(spec, shapes, strides, dtype=dtype, mode=mode,
+                             out_strides=out_strides, chain_order=chain_order)
+
+
+@functools.lru_cache(maxsize=4096)
+def _plan_cached(spec, shapes, strides, dtype, mode, out_strides, chain_order):
+    return _plan_generic(spec, shapes, strides, dtype=dtype, mode=mode, out_strides=out_strides,
+                         chain_order=chain_order)
+
+
+def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
+                  out_strides=None, chain_order: str = "left"):
     n_in = len(spec.inputs)
     ext = extents_of(spec, shapes)
     all_par = all(a in spec.output for a in spec.axes)
