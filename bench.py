@@ -515,7 +515,10 @@ def main():
     aux = None
     cpu = None
     if not args.no_aux and (world == 1 or backend == "nccl"):
-        ks = ksplit_aux(dev, world, rank)
+        try:
+            ks = ksplit_aux(dev, world, rank)
+        except Exception as e:  # an aux line must never sink the headline
+            ks = {"error": f"{type(e).__name__}: {e}"[:300]}
         aux = {"ksplit_fused_reduce_scatter": ks}
     if rank == 0 and world == 1:
         if not args.no_aux:
