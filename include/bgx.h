@@ -85,6 +85,8 @@ BGX_API int bgx_permute(const bgx_tensor *in, const bgx_tensor *out,
  * walks that element's reduction sub-space in the reference's lexicographic
  * order, p = x1; p = p*xk (k = 2..n); acc = p + acc, each op separately
  * rounded (no FMA).  Bit-identical to the reference for f32 and f64.
+ * bf16/f16 (DSL extension): operands widened to f32, the same loop in f32,
+ * one final round-to-nearest-even to the storage type.
  * Axes: [0, n_par) are the output (parallel) axes in output order, then the
  * reduction axes (einsum.py:81).  c0 and out are dense row-major over the
  * parallel axes; c0 may equal out.  passthrough = (n_in == 1 && no reduction). */
@@ -92,7 +94,7 @@ typedef struct {
   int32_t n_in;
   int32_t n_axes;
   int32_t n_par;
-  int32_t dtype;                                   /* BGX_F32 or BGX_F64  */
+  int32_t dtype;                       /* BGX_F32, BGX_F64, BGX_BF16, BGX_F16 */
   int64_t extents[BGX_MAX_AXES];
   const void *ins[BGX_MAX_OPERANDS];
   int64_t strides[BGX_MAX_OPERANDS][BGX_MAX_AXES]; /* 0 = axis not indexed */

@@ -8,7 +8,10 @@
 // sub-space in the same lexicographic order with an odometer, forms
 // p = x1 * x2 * ... (left fold) and acc = p + acc with __fmul_rn/__fadd_rn
 // (no FMA contraction, no flush-to-zero), so every output is bit-identical to
-// the reference.  This is the kernel for bodies the GEMM planner does not map
+// the reference.  bf16/f16 operands (the DSL extension)
+// use the tensor-core path's semantics: values are widened to f32, the same
+// loop runs in f32 with per-op rounding, and the result is rounded once to the
+// storage type (round-to-nearest-even).  This is the kernel for bodies the GEMM planner does not map
 // (single-input reductions, Hadamard/outer products, 3+-operand patterns,
 // rank-0 outputs) and for fp32 parity runs.
 #include "common.cuh"
@@ -23,7 +26,19 @@ template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
 template <> __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
 template <> __device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
 
-template <typename T, int NIN>
+// storage type S, arithmetic type T (T = S for f32/f64, float for bf16/f16)
+template <typename S, typename T> __device__ __forceinline__ T ld_as(const S *p) {
+  return Conv<S>::to_f(*p);
+}
+template <> __device__ __forceinline__ float ld_as<float, float>(const float *p) { return *p; }
+template <> __device__ __forceinline__ double ld_as<double, double>(const double *p) { return *p; }
+template <typename S, typename T> __device__ __forceinline__ S st_as(T v) {
+  return Conv<S>::from_f(v);
+}
+template <> __device__ __forceinline__ float st_as<float, float>(float v) { return v; }
+template <> __device__ __forceinline__ double st_as<double, double>(double v) { return v; }
+
+template <typename S, typename T, int NIN>
 __global__ void __launch_bounds__(128)
 generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
   const int n_in = NIN > 0 ? NIN : d.n_in;
@@ -41,20 +56,21 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
       rem /= e;
       for (int k = 0; k < n_in; ++k) off[k] += i * d.strides[k][a];
     }
-    const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+    const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+    S *out = static_cast<S *>(d.out);
     if (passthrough) {
-      static_cast<T *>(d.out)[o] = ins[0][off[0]];
+      out[o] = ins[0][off[0]];
       continue;
     }
-    T acc = static_cast<const T *>(d.c0)[o];
+    T acc = ld_as<S, T>(static_cast<const S *>(d.c0) + o);
     if (red_points == 0) {
-      static_cast<T *>(d.out)[o] = acc;
+      out[o] = st_as<S, T>(acc);
       continue;
     }
     if (n_red == 0) {  // elementwise body (Hadamard / outer product): one point
-      T p = ins[0][off[0]];
-      for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k]]);
-      static_cast<T *>(d.out)[o] = add_rn<T>(p, acc);
+      T p = ld_as<S, T>(ins[0] + off[0]);
+      for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ld_as<S, T>(ins[k] + off[k]));
+      out[o] = st_as<S, T>(add_rn<T>(p, acc));
       continue;
     }
     // Innermost reduction axis: U points of every operand are loaded ahead
@@ -75,9 +91,9 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
 #pragma unroll
         for (int k = 0; k < (NIN > 0 ? NIN : BGX_MAX_OPERANDS); ++k) {
           if (k >= n_in) break;
-          const T *base = ins[k] + off[k] + j * sin[k];
+          const S *base = ins[k] + off[k] + j * sin[k];
 #pragma unroll
-          for (int u = 0; u < U; ++u) v[k][u] = base[u * sin[k]];
+          for (int u = 0; u < U; ++u) v[k][u] = ld_as<S, T>(base + u * sin[k]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -87,8 +103,8 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
         }
       }
       for (; j < E; ++j) {
-        T p = ins[0][off[0] + j * sin[0]];
-        for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k] + j * sin[k]]);
+        T p = ld_as<S, T>(ins[0] + off[0] + j * sin[0]);
+        for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ld_as<S, T>(ins[k] + off[k] + j * sin[k]));
         acc = add_rn<T>(p, acc);
       }
       // odometer over the outer reduction axes (last of them fastest)
@@ -102,21 +118,21 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
         idx[a] = 0;
       }
     }
-    static_cast<T *>(d.out)[o] = acc;
+    out[o] = st_as<S, T>(acc);
   }
 }
 
-template <typename T>
+template <typename S, typename T>
 int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
   const int sms = sm_count_current();
   if (sms <= 0) { set_error("bgx_generic: no device"); return BGX_ERR_NO_DEVICE; }
   int64_t blocks = (n_out + 127) / 128;
   if (blocks > (int64_t)sms * 64) blocks = (int64_t)sms * 64;
   switch (d.n_in) {
-    case 1: generic_kernel<T, 1><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
-    case 2: generic_kernel<T, 2><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
-    case 3: generic_kernel<T, 3><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
-    default: generic_kernel<T, 0><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 1: generic_kernel<S, T, 1><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 2: generic_kernel<S, T, 2><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 3: generic_kernel<S, T, 3><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+    default: generic_kernel<S, T, 0><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
   }
   return check_launch("generic_kernel");
 }
@@ -132,8 +148,9 @@ extern "C" int bgx_generic(const bgx_generic_desc *d, void *stream) {
   BGX_CHECK_ARG(d->n_axes >= 0 && d->n_axes <= BGX_MAX_AXES && d->n_par >= 0 &&
                     d->n_par <= d->n_axes,
                 "bgx_generic: axes %d / parallel %d", d->n_axes, d->n_par);
-  BGX_CHECK_ARG(d->dtype == BGX_F32 || d->dtype == BGX_F64,
-                "bgx_generic: dtype %d (the reference body types are f32/f64)", d->dtype);
+  BGX_CHECK_ARG(d->dtype == BGX_F32 || d->dtype == BGX_F64 || d->dtype == BGX_BF16 ||
+                    d->dtype == BGX_F16,
+                "bgx_generic: dtype %d", d->dtype);
   int64_t n_out = 1, red = 1;
   for (int a = 0; a < d->n_axes; ++a) {
     BGX_CHECK_ARG(d->extents[a] >= 0, "bgx_generic: negative extent");
@@ -146,6 +163,10 @@ extern "C" int bgx_generic(const bgx_generic_desc *d, void *stream) {
   if (red > 0 || passthrough)
     for (int k = 0; k < d->n_in; ++k) BGX_CHECK_ARG(d->ins[k] != nullptr, "bgx_generic: null input");
   cudaStream_t s = (cudaStream_t)stream;
-  if (d->dtype == BGX_F32) return launch_generic<float>(*d, n_out, red, s);
-  return launch_generic<double>(*d, n_out, red, s);
+  switch (d->dtype) {
+    case BGX_F32: return launch_generic<float, float>(*d, n_out, red, s);
+    case BGX_F64: return launch_generic<double, double>(*d, n_out, red, s);
+    case BGX_BF16: return launch_generic<__nv_bfloat16, float>(*d, n_out, red, s);
+    default: return launch_generic<__half, float>(*d, n_out, red, s);
+  }
 }

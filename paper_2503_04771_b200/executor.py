@@ -105,10 +105,12 @@ def permute(x: torch.Tensor, out: torch.Tensor, perm) -> torch.Tensor:
 
 
 def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor) -> torch.Tensor:
-    """The reference loop nest on the device (bit-exact, f32/f64)."""
+    """The reference loop nest on the device (bit-exact for f32/f64; bf16/f16
+    widened to f32, per-op f32 rounding, one final rounding to the storage
+    type — the tensor-core path's semantics)."""
     lib = _lib.load()
-    if out.dtype not in (torch.float32, torch.float64):
-        raise NotImplementedError("bgx_generic computes in the reference's f32/f64 only")
+    if out.dtype not in TORCH_TO_BGX:
+        raise NotImplementedError(f"bgx_generic: unsupported dtype {out.dtype}")
     if len(inputs) > _lib.MAX_OPERANDS or len(spec.axes) > _lib.MAX_AXES:
         raise NotImplementedError("bgx_generic: too many operands/axes")
     d = _lib.BgxGenericDesc()

@@ -69,8 +69,6 @@ class Prepared:
                 return self._lib.bgx_permute(ti, to, perm, torch.cuda.current_stream().cuda_stream)
             return run
         if isinstance(p, GenericPlan) and out.is_contiguous() and (self.c0 is None or self.c0.is_contiguous()):
-            if out.dtype not in (torch.float32, torch.float64):
-                return None
             d = _lib.BgxGenericDesc()
             d.n_in, d.n_axes, d.n_par = len(ins), len(spec.axes), len(spec.output)
             d.dtype = executor.TORCH_TO_BGX[out.dtype]

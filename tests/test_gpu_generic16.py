@@ -1,0 +1,67 @@
+"""bf16/f16 bodies the GEMM planner does not map (reductions, Hadamard and
+outer products, rank-0 outputs, passthrough, 3-operand bodies) through the
+reference-shaped API and ``contract``: the generic kernel widens to f32, runs
+the reference's loop order with per-op f32 rounding and rounds once — so it
+is bit-equal to the C oracle on the f32-widened inputs followed by one
+round-to-nearest-even to the storage type."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2503_04771_b200 import einsum as E
+from paper_2503_04771_b200 import executor
+from paper_2503_04771_b200 import interp as I
+from paper_2503_04771_b200.api import contract
+
+pytestmark = pytest.mark.gpu
+
+SPECS = ["(i,j)->(i)", "(i,j)->(j)", "(i,j)->()", "(i,j),(i,j)->(i,j)", "(i),(j)->(i,j)",
+         "(i,j,k)->(k,i)", "(i,k),(k,j),(j)->(i)", "(i)->(i)", "(b,i,j),(b,j)->(b,i)"]
+
+
+def _shapes(spec, ext):
+    return [tuple(ext[x] for x in t) for t in spec.inputs], tuple(ext[x] for x in spec.output)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("text", SPECS)
+def test_generic16_matches_widened_oracle(dev, text, dtype):
+    spec = E.parse_einsum(text)
+    rng = np.random.default_rng(len(text))
+    ext = {a: int(rng.integers(3, 40)) for a in spec.axes}
+    in_shapes, out_shape = _shapes(spec, ext)
+    ins = [torch.from_numpy(rng.standard_normal(s).astype(np.float32)).to(dtype) for s in in_shapes]
+    c0 = torch.from_numpy(rng.standard_normal(out_shape).astype(np.float32)).to(dtype)
+    executor.reset_launch_log()
+    got = contract(spec, *[t.to(dev) for t in ins], c0=c0.to(dev))
+    if text == "(i)->(i)":
+        assert torch.equal(got.cpu(), ins[0])
+        return
+    want32 = oracle.generic(list(spec.inputs), spec.output, [t.float().numpy() for t in ins],
+                            c0.float().numpy())
+    want = torch.from_numpy(np.asarray(want32, np.float32)).to(dtype)
+    if executor.launch_log() != ["generic"]:
+        # GEMM-shaped 16-bit bodies (incl. GEMV and multi-operand chains) run
+        # on the GEMM kernels (f32 accumulate with FMA / tensor cores, 16-bit
+        # intermediates between chain steps): tolerance, not bits
+        w = want32.astype(np.float64)
+        relf = float(np.linalg.norm(got.cpu().double().numpy() - w) / np.linalg.norm(w))
+        assert relf <= 1e-2, (text, relf)
+        return
+    assert torch.equal(got.cpu().view(torch.int16), want.view(torch.int16)), text
+
+
+def test_generic16_through_run_function(dev):
+    spec = E.parse_einsum("(i,j)->(i)")
+    mod = E.build_einsum_function(None, spec, elem=E.BF16)
+    x = torch.randn(17, 300, device=dev).bfloat16()
+    z = torch.zeros(17, device=dev, dtype=torch.bfloat16)
+    executor.reset_launch_log()
+    [got] = I.run_function(mod, "einsum", [I.TensorValue(E.BF16, x.shape, x),
+                                          I.TensorValue(E.BF16, z.shape, z)], step_limit=None)
+    assert executor.launch_log() == ["generic"]
+    want = torch.from_numpy(np.asarray(oracle.generic([("i", "j")], ("i",), [x.float().cpu().numpy()],
+                                                      np.zeros(17, np.float32)), np.float32))
+    assert torch.equal(got.data.cpu().float(), want.bfloat16().float())
