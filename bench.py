@@ -63,11 +63,13 @@ def peaks():
 # clocks during the timed region (NVML, sampled from a thread)
 
 class ClockSampler:
+    """NVML SM clock, clock-event reasons and board power, sampled every few ms
+    on a thread while the timed region runs (the recipe's clocks line)."""
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int, period_s: float = 0.005):
-        self.samples, self.reasons = [], set()
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.power, self.errors = [], {}, [], []
         self.max_mhz = None
         self.period = period_s
         self._stop = threading.Event()
@@ -77,23 +79,37 @@ class ClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
+        except Exception as e:  # noqa: BLE001
             self.nv = None
+            self.errors.append(repr(e))
+
+    def _sample(self):
+        nv, h = self.nv, self.h
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.errors.append(repr(e))
+        try:
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            for bit, name in self.REASONS.items():
+                if mask & bit:
+                    self.reasons[name] = self.reasons.get(name, 0) + 1
+        except Exception as e:  # noqa: BLE001
+            self.errors.append(repr(e))
+        try:
+            self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+        except Exception as e:  # noqa: BLE001
+            self.errors.append(repr(e))
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            self._sample()
             time.sleep(self.period)
+        self._sample()   # one sample at the very end of the timed region
 
     def __enter__(self):
         if self.nv:
+            self._sample()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         return self
@@ -105,9 +121,31 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"],
+                    "errors": self.errors[:2]}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples),
+               "reason_samples": dict(sorted(self.reasons.items())),
+               "power_w_median": statistics.median(self.power) if self.power else None,
+               "power_w_max": max(self.power) if self.power else None}
+        if self.errors:
+            out["errors"] = sorted(set(self.errors))[:2]
+        return out
+
+
+def inband_clock(buf) -> dict:
+    """Average SM clock over the timed region from two bgx_clock_sample
+    snapshots (per SM: delta %clock64 / delta %globaltimer)."""
+    before = {int(r[0]): (int(r[1]), int(r[2])) for r in buf[0].reshape(-1, 3)}
+    after = {int(r[0]): (int(r[1]), int(r[2])) for r in buf[1].reshape(-1, 3)}
+    mhz = [(after[s][0] - before[s][0]) * 1e3 / (after[s][1] - before[s][1])
+           for s in before if s in after and after[s][1] > before[s][1]]
+    if not mhz:
+        return {"sm_mhz_inband": None}
+    mhz.sort()
+    return {"sm_mhz_inband": round(mhz[len(mhz) // 2], 1), "sm_mhz_inband_min": round(mhz[0], 1),
+            "sm_mhz_inband_max": round(mhz[-1], 1), "inband_sms": len(mhz),
+            "inband_note": "per-SM delta %clock64 / delta %globaltimer across the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -444,13 +482,21 @@ def main():
     barrier_sync(world)
     executor.reset_launch_log()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nsm = _lib.load().bgx_sm_count()
+    clk_buf = torch.zeros(2, nsm * 3, dtype=torch.int64, device=dev)
     with ClockSampler(local_dev) as clk:
+        _lib.check(_lib.load().bgx_clock_sample(clk_buf[0].data_ptr(), stream.cuda_stream),
+                   "bgx_clock_sample")
         t0.record(stream)
         for _ in range(args.steps):
             step(record=True)
         t1.record(stream)
+        _lib.check(_lib.load().bgx_clock_sample(clk_buf[1].data_ptr(), stream.cuda_stream),
+                   "bgx_clock_sample")
         torch.cuda.synchronize()
     launches = len(executor.launch_log())
+    clocks = clk.summary()
+    clocks.update(inband_clock(clk_buf.cpu().numpy()))
     barrier_sync(world)
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = max_over_ranks(ms_local, world)
@@ -554,7 +600,7 @@ def main():
             "parity": {"relF_row_samples_max_over_ranks": relF, "tolerance": 1e-2,
                        "oracle": "float64 (A@B)@C on the bf16 inputs"},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "clocks": clk.summary(), "aux": aux,
+            "clocks": clocks, "aux": aux,
         }
         print(json.dumps(line))
     if world > 1:

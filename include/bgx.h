@@ -235,6 +235,12 @@ BGX_API int bgx_contract_reduce_scatter(const bgx_contract_desc *d, const bgx_re
 BGX_API int bgx_cast_f32(const float *src, const void *c0, void *out, int32_t out_dtype,
                  int64_t n, void *stream);
 
+/* ---- measurement -----------------------------------------------------------
+ * One CTA per SM writes (smid, %clock64, %globaltimer) to out[3 * sm_count]
+ * (device memory).  Two samples around a timed region give every SM's
+ * average clock over it (bench.py's in-band clocks figure).                */
+BGX_API int bgx_clock_sample(uint64_t *out, void *stream);
+
 /* ---- runtime-compiled kernels (GPU case study) ---------
  * Replaces the simulated sequential thread grid of bridgegen run_kernel
  * (interp.py:434-461): CUDA C generated from an IR kernel is compiled with

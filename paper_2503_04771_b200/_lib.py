@@ -96,6 +96,7 @@ SIGNATURES = {
     "bgx_contract_reduce_scatter": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
                                                    ctypes.POINTER(BgxReduceScatter), _vp]),
     "bgx_cast_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _vp]),
+    "bgx_clock_sample": (ctypes.c_int, [_vp, _vp]),
     "bgx_rtc_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p,
                                        ctypes.POINTER(_vp), ctypes.c_char_p, _i64]),
     "bgx_rtc_launch": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32,

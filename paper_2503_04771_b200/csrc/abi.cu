@@ -44,6 +44,23 @@ __global__ void cast_f32_kernel(const float *__restrict__ src, const OutT *__res
   }
 }
 
+// One CTA per SM (the dynamic shared memory request forces it): record
+// (smid, %clock64, %globaltimer).  Two samples around a timed region give
+// each SM's average clock over it — the in-band measurement of the clock the
+// work actually ran at (NVML's clock reading is refreshed too slowly for a
+// region of ~100 ms).
+__global__ void clock_sample_kernel(uint64_t *out) {
+  if (threadIdx.x != 0) return;
+  uint32_t smid;
+  uint64_t clk, ns;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(clk));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  out[blockIdx.x * 3 + 0] = smid;
+  out[blockIdx.x * 3 + 1] = clk;
+  out[blockIdx.x * 3 + 2] = ns;
+}
+
 }  // namespace bgx
 
 using namespace bgx;
@@ -88,6 +105,23 @@ int bgx_cast_f32(const float *src, const void *c0, void *out, int32_t out_dtype,
       return BGX_ERR_UNSUPPORTED;
   }
   return check_launch("cast_f32_kernel");
+}
+
+int bgx_clock_sample(uint64_t *out, void *stream) {
+  BGX_CHECK_ARG(out != nullptr, "bgx_clock_sample: null output");
+  const int sms = sm_count_current();
+  if (sms <= 0) { set_error("bgx_clock_sample: no device"); return BGX_ERR_NO_DEVICE; }
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  constexpr int SMEM = 200 * 1024;   // > half an SM's shared memory: one CTA per SM
+  if (!configured[dev & 63]) {
+    BGX_CUDA_TRY(cudaFuncSetAttribute(clock_sample_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    configured[dev & 63] = 1;
+  }
+  clock_sample_kernel<<<(unsigned)sms, 32, SMEM, (cudaStream_t)stream>>>(out);
+  return check_launch("clock_sample_kernel");
 }
 
 }  // extern "C"
