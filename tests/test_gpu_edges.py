@@ -68,3 +68,22 @@ def test_errors_raise_without_fallback(dev):
         contract("(i,k),(k,j)->(i,j)", torch.zeros(4, 3), torch.zeros(3, 5))
     with pytest.raises(E.EinsumError):
         contract("ij,jk->ik", torch.zeros(4, 3, device=dev), torch.zeros(3, 5, device=dev))
+
+
+def test_clock_sample_one_cta_per_sm(dev):
+    """bgx_clock_sample: one record per SM (distinct smids), clocks advance and
+    the derived frequency is physical."""
+    from paper_2503_04771_b200 import _lib
+    lib = _lib.load()
+    n = lib.bgx_sm_count()
+    buf = torch.zeros(2, n * 3, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.bgx_clock_sample(buf[0].data_ptr(), st), "clock")
+    torch.cuda._sleep(50_000_000)
+    _lib.check(lib.bgx_clock_sample(buf[1].data_ptr(), st), "clock")
+    torch.cuda.synchronize()
+    h = buf.cpu().numpy().reshape(2, n, 3)
+    assert len(set(h[0, :, 0].tolist())) == n and len(set(h[1, :, 0].tolist())) == n
+    import bench
+    c = bench.inband_clock(buf.cpu().numpy())
+    assert c["inband_sms"] == n and 200 < c["sm_mhz_inband"] < 2500
