@@ -536,7 +536,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       uint32_t *tcount = tail ? p.tail_counters + (t - p.tail_start) * CG + rank : nullptr;
       const int acc = it % C::ACC_BUFS;
       const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
-      mbar_wait(&tmem_full[acc], acc_phase);
+      // One epilogue warp polls the accumulator barrier; the other seven wait
+      // in a named barrier, which issues nothing (ncu: with all eight warps
+      // polling, the wait loop was half of the kernel's instructions — issue
+      // energy on a power-capped part)
+      if (ew == 0) mbar_wait(&tmem_full[acc], acc_phase);
+      named_bar_sync(2, 32 * EPI_WARPS);
       tc_fence_after();
       constexpr bool SPLIT_RELEASE = C::ACC_BUFS == 1 && C::NSPLIT == 2;
       auto arrive_empty = [&](int which) {
@@ -978,10 +983,44 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   return check_launch("tc_gemm_kernel");
 }
 
+// Co-resident 4-CTA clusters of the A-multicast kernel (a 4-CTA cluster must
+// fit in one GPC: 33 on a 148-SM B200, i.e. 132 SMs busy), cached per device.
+template <int BN, typename OutT>
+int cn2_slots() {
+  using C = Cfg<BN, 2, (int)sizeof(OutT), 2>;
+  static thread_local int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!cache[dev & 63]) {
+    auto kern = tc_gemm_kernel<BN, 2, OutT, 2, false, 2>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      cache[dev & 63] = -1;
+    } else {
+      const int n = max_clusters(kern, C::SMEM_BYTES, 4);
+      cache[dev & 63] = n > 0 ? n : -1;
+    }
+  }
+  return cache[dev & 63];
+}
+
 template <int CG, typename OutT, int IB = 2>
 int dispatch_bn(const bgx_contract_desc &d, int bn, const TcParams &p, cudaStream_t s,
                 int cn = 1) {
   if constexpr (CG == 2 && IB == 2) {
+    // automatic A multicast: only when the 4-CTA clusters (fewer SMs, but a
+    // quarter less L2->SM traffic per flop, hence higher clocks under the
+    // power cap) need no more waves than CTA pairs do — e.g. 4096^3
+    if (cn == 0 && (bn == 256 || bn == 512) && p.k_splits <= 1 && p.tail_splits <= 1) {
+      const int64_t tm = (d.M + 255) / 256, tn = (d.N + bn - 1) / bn;
+      const int64_t tiles = tm * tn * d.batch, units = tm * ((tn + 1) / 2) * d.batch;
+      const int64_t slots2 = sm_count_current() / 2;
+      const int64_t slots4 = bn == 512 ? cn2_slots<512, OutT>() : cn2_slots<256, OutT>();
+      if (slots4 > 0 && (units + slots4 - 1) / slots4 <= (tiles + slots2 - 1) / slots2 &&
+          tiles >= slots2)
+        cn = 2;
+    }
     if (cn == 2 && bn == 512) return launch_tc<512, 2, OutT, 2, false, 2>(d, p, s);
     if (cn == 2 && bn == 256) return launch_tc<256, 2, OutT, 2, false, 2>(d, p, s);
   }
@@ -1110,8 +1149,10 @@ int contract_tc_impl(const bgx_contract_desc &d, int splits, cudaStream_t s, int
   p.raster = d.sched.raster != 0 ? d.sched.raster : (bn == 512 ? -8 : (cg == 2 ? 8 : 16));
   p.debug = d.sched.reserved[0];
   // two CTA pairs per cluster sharing A by multicast (schedule reserved[1]
-  // = cluster_n; not with the tail split, whose workspace slots are per unit)
-  const int cn = (cg == 2 && d.sched.reserved[1] == 2 && tail_splits <= 1) ? 2 : 1;
+  // = cluster_n: 0 automatic, 1 off, 2 on; never with the tail split, whose
+  // workspace slots are per unit)
+  const int cn = (cg != 2 || tail_splits > 1 || d.sched.reserved[1] == 1) ? 1
+                 : d.sched.reserved[1] == 2 ? 2 : 0;
   if (d.in_dtype == BGX_F32)  // tf32 tensor cores (opt-in BGX_MODE_TF32)
     return cg == 2 ? dispatch_bn<2, float, 4>(d, bn, p, s) : dispatch_bn<1, float, 4>(d, bn, p, s);
   if (d.out_dtype == BGX_F32)

@@ -324,7 +324,7 @@ def test_cluster_n2_a_multicast_bit_equal(dev, M, N, K, bn, a_mn, b_mn):
     b_in = b if b_mn else b.t().contiguous().t()
     for out_dtype, c0 in ((torch.bfloat16, None), (torch.float32, torch.randn(M, N, device=dev))):
         base = contract("(i,k),(k,j)->(i,j)", a_in, b_in, out_dtype=out_dtype, c0=c0,
-                        schedule={"tile_n": bn, "cta_group": 2, "no_splitk": 1})
+                        schedule={"tile_n": bn, "cta_group": 2, "cluster_n": 1, "no_splitk": 1})
         y = contract("(i,k),(k,j)->(i,j)", a_in, b_in, out_dtype=out_dtype, c0=c0,
                      schedule={"tile_n": bn, "cta_group": 2, "cluster_n": 2, "no_splitk": 1})
         assert torch.equal(y, base)
@@ -336,6 +336,16 @@ def test_cluster_n2_batched(dev):
     a = torch.randn(6, 384, 512, device=dev).half()
     b = torch.randn(6, 512, 640, device=dev).half()
     sc = {"tile_n": 256, "cta_group": 2}
-    base = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, schedule=sc)
+    base = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, schedule=dict(sc, cluster_n=1))
     y = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, schedule=dict(sc, cluster_n=2))
     assert torch.equal(y, base)
+
+
+def test_auto_cluster_choice_is_bit_equal(dev):
+    """4096^3: the automatic choice (A-multicast clusters when they need no
+    more waves) gives exactly the single-pair result."""
+    a = torch.randn(4096, 4096, device=dev).bfloat16()
+    b = torch.randn(4096, 4096, device=dev).bfloat16()
+    auto = contract("(i,k),(k,j)->(i,j)", a, b)
+    one = contract("(i,k),(k,j)->(i,j)", a, b, schedule={"cluster_n": 1})
+    assert torch.equal(auto, one)
