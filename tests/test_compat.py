@@ -143,3 +143,22 @@ def test_chained_generics_through_reference_builder(registry, dev):
         [got] = interp.run_function(module, "twice", [tv(a), tv(b), tv(zero)])
     assert G.bits_equal(got.data, ref.data)
     assert np.allclose(got.data, (a @ b) @ b, rtol=1e-4)
+
+
+@pytest.mark.gpu
+def test_schedule_string_attr_on_reference_op(registry, dev):
+    """A ``bgx.schedule`` StringAttr on a real bridgegen linalg.generic pins the
+    tensor-core tile (tf32 mode; the exact f32 default ignores schedules)."""
+    mod = einsum.build_einsum_function(registry, einsum.parse_einsum("(i,k),(k,j)->(i,j)"))
+    op = generic_of(mod)
+    op.attributes["bgx.schedule"] = ir.StringAttr("tile_n=128,cta_group=1")
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal((512, 256)).astype(np.float32)
+    b = rng.standard_normal((256, 384)).astype(np.float32)
+    c = np.zeros((512, 384), np.float32)
+    with compat.backend("tf32"):
+        executor.reset_launch_log()
+        [got] = interp.run_function(mod, "einsum", [tv(a), tv(b), tv(c)], step_limit=10 ** 9)
+    assert executor.tile_log() and executor.tile_log()[-1][:2] == (1, 128)
+    want = a.astype(np.float64) @ b.astype(np.float64)
+    assert np.linalg.norm(got.data - want) / np.linalg.norm(want) < 5e-3
