@@ -35,14 +35,21 @@ def output_shape(spec: EinsumSpec, operands) -> tuple:
 def contract(spec, *operands: torch.Tensor, out: torch.Tensor | None = None,
              c0: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
              mode: str = "auto", schedule=None,
-             chain_order: str = "left") -> torch.Tensor:
+             chain_order: str = "left", devices=None) -> torch.Tensor:
     """Evaluate an einsum spec such as ``"(i,k),(k,j)->(i,j)"`` on CUDA tensors.
 
     ``c0``: initial output (the reference's output operand; None = zeros).
     ``out``: optional preallocated result (may alias nothing else).
     ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt' (include/bgx.h).
     ``schedule``: optional ``Schedule`` / dict / ``"tile_n=512,cta_group=2"``.
-    ``chain_order``: 'left' or 'optimal' pairwise order for 3+ inputs."""
+    ``chain_order``: 'left' or 'optimal' pairwise order for 3+ inputs.
+    ``devices``: list of CUDA devices — M-shard the contraction over them from
+    this one process (``shard.contract_devices``)."""
+    if devices is not None and len(devices) > 1:
+        from .shard import contract_devices
+        return contract_devices(spec, *operands, devices=devices, out=out, c0=c0,
+                                out_dtype=out_dtype, mode=mode, schedule=schedule,
+                                chain_order=chain_order)
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
     from .schedule import as_schedule_dict

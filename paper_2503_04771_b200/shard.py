@@ -286,3 +286,50 @@ def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> 
         _lib.check(lib.bgx_contract_reduce_scatter(dr, rs, stream), "bgx_contract_reduce_scatter")
         executor._log("tcgen05-rs")
     return out[:M]
+
+
+# ---------------------------------------------------------------------------
+# one process, several devices (``einsum(..., devices=...)``)
+
+def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> torch.Tensor:
+    """M-sharded contraction driven from ONE process over ``devices``: rows of
+    the output's leading index (which must come only from operand 0) are split
+    into contiguous slabs (``row_range``); slab r of operand 0 and a replica
+    of every other operand go to ``devices[r]`` (peer copies over NVLink), each
+    device contracts its slab on its own current stream — launches are
+    asynchronous, so the devices run concurrently — and the slabs are copied
+    back into ``out`` on the operands' device.  No collective: the slabs are
+    independent (the §8e M-shard), so the result equals the single-device one
+    row for row."""
+    from .api import _row_streamable, output_shape
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
+    if not _row_streamable(spec, operands):
+        raise ValueError(f"{spec}: the output's leading index must come from operand 0 only")
+    home = operands[0].device
+    shape = output_shape(spec, operands)
+    dt = kw.get("out_dtype") or operands[0].dtype
+    if out is None:
+        out = torch.empty(shape, dtype=dt, device=home)
+    c0 = kw.pop("c0", None)
+    rows = shape[0]
+    n = len(devices)
+    pending = []
+    for r, dev in enumerate(devices):
+        lo, hi = row_range(rows, n, r)
+        if hi <= lo:
+            continue
+        with torch.cuda.device(dev):
+            a = operands[0][lo:hi].to(dev, non_blocking=True)
+            others = [t.to(dev, non_blocking=True) for t in operands[1:]]
+            cc = c0[lo:hi].to(dev, non_blocking=True) if c0 is not None else None
+            y = contract(spec, a, *others, c0=cc, **kw)
+            done = torch.cuda.Event()
+            done.record(torch.cuda.current_stream(dev))
+        pending.append((lo, hi, y, done))
+    home_stream = torch.cuda.current_stream(home)
+    for lo, hi, y, done in pending:
+        home_stream.wait_event(done)
+        out[lo:hi].copy_(y, non_blocking=True)
+    return out

@@ -42,3 +42,18 @@ def test_chunked_host_fp32_exact_with_c0(dev):
     got = contract_host("(i,k),(k,j)->(i,j)", a, b, c0=c0, device=dev, chunk_rows=128)
     want = oracle.gemm_kseq(a.numpy(), b.numpy(), c0.numpy())
     assert np.array_equal(got.numpy(), want)
+
+
+def test_contract_devices_matches_single_device(dev):
+    """One-process M-shard over a device list (here the same GPU twice and
+    three times): bit-identical rows to the unsharded call."""
+    a = torch.randn(3000, 1024, device=dev).bfloat16()
+    b = torch.randn(1024, 768, device=dev).bfloat16()
+    c = torch.randn(768, 512, device=dev).bfloat16()
+    spec = "(i,k),(k,j),(j,l)->(i,l)"
+    whole = contract(spec, a, b, c, schedule={"splits": 1})
+    for devs in ([0, 0], [0, 0, 0]):
+        sh = contract(spec, a, b, c, devices=devs, schedule={"splits": 1})
+        assert torch.equal(sh, whole)
+    with pytest.raises(ValueError, match="leading index"):
+        contract("(k,i),(k,j)->(i,j)", a.t(), b, devices=[0, 0])
