@@ -349,3 +349,32 @@ def test_auto_cluster_choice_is_bit_equal(dev):
     auto = contract("(i,k),(k,j)->(i,j)", a, b)
     one = contract("(i,k),(k,j)->(i,j)", a, b, schedule={"cluster_n": 1})
     assert torch.equal(auto, one)
+
+
+def test_tail_split_batched_and_f16(dev):
+    """Tail split with a batch index and fp16 in/out: matches the unsplit
+    kernel to f32 noise and is deterministic."""
+    a = torch.randn(3, 1280, 2048, device=dev).half()
+    b = torch.randn(3, 2048, 1536, device=dev).half()
+    spec = "(b,i,k),(b,k,j)->(b,i,j)"
+    plain = contract(spec, a, b, out_dtype=torch.float32, schedule={"splits": 1})
+    for sp in (-2, -3):
+        executor.reset_launch_log()
+        tail = contract(spec, a, b, out_dtype=torch.float32, schedule={"splits": sp})
+        assert executor.launch_log() == ["tcgen05-tailsplit"], executor.launch_log()
+        assert float((tail - plain).norm() / plain.norm()) <= 1e-6
+        again = contract(spec, a, b, out_dtype=torch.float32, schedule={"splits": sp})
+        assert torch.equal(tail, again)
+
+
+def test_cluster_n2_with_uniform_splitk(dev):
+    """A-multicast clusters combined with uniform split-K slices."""
+    a = torch.randn(512, 65536, device=dev).bfloat16()
+    b = torch.randn(65536, 1024, device=dev).bfloat16()
+    sc = {"tile_n": 256, "cta_group": 2, "splits": 4}
+    base = contract("(i,k),(k,j)->(i,j)", a, b, out_dtype=torch.float32,
+                    schedule=dict(sc, cluster_n=1))
+    executor.reset_launch_log()
+    y = contract("(i,k),(k,j)->(i,j)", a, b, out_dtype=torch.float32, schedule=dict(sc, cluster_n=2))
+    assert executor.launch_log() == ["tcgen05-splitk"]
+    assert torch.equal(y, base)
