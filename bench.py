@@ -561,10 +561,28 @@ def main():
     aux = None
     cpu = None
     if not args.no_aux and (world == 1 or backend == "nccl"):
-        try:
-            ks = ksplit_aux(dev, world, rank)
-        except Exception as e:  # an aux line must never sink the headline
-            ks = {"error": f"{type(e).__name__}: {e}"[:300]}
+        ok, why = True, ""
+        if world > 1:
+            # every rank must agree that symmetric memory works before any
+            # rank enters the fused path's collectives (no rank may be left
+            # waiting in a barrier the others never reach)
+            try:
+                from torch.distributed import _symmetric_memory as symm_mem
+                probe = symm_mem.empty(64, dtype=torch.uint8, device=dev)
+                symm_mem.rendezvous(probe, dist.group.WORLD)
+            except Exception as e:  # noqa: BLE001
+                ok, why = False, f"{type(e).__name__}: {e}"[:200]
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                ok, why = False, why or "symmetric memory unavailable on another rank"
+        if ok:
+            try:
+                ks = ksplit_aux(dev, world, rank)
+            except Exception as e:  # an aux line must never sink the headline
+                ks = {"error": f"{type(e).__name__}: {e}"[:300]}
+        else:
+            ks = {"skipped": why}
         aux = {"ksplit_fused_reduce_scatter": ks}
     if rank == 0 and world == 1:
         if not args.no_aux:
