@@ -279,9 +279,7 @@ simt_gemm_big_kernel(const Params p) {
     const int buf = kt & 1;
     if (kt + 1 < ktiles) load_tiles((kt + 1) * BKB);   // in flight during the math
     const int kmax = (p.K - kt * BKB) < BKB ? (int)(p.K - kt * BKB) : BKB;
-#pragma unroll
-    for (int kk = 0; kk < BKB; ++kk) {
-      if (kk >= kmax) break;
+    auto kstep = [&](int kk) {
       Acc av[8], bv[8];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -294,6 +292,14 @@ simt_gemm_big_kernel(const Params p) {
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = Arith<Acc>::template mac<FUSED>(av[i], bv[j], acc[i][j]);
+    };
+    if (kmax == BKB) {
+      // full k-tile: straight-line code, so the compiler can issue the next
+      // step's shared loads under the current step's FMAs
+#pragma unroll
+      for (int kk = 0; kk < BKB; ++kk) kstep(kk);
+    } else {
+      for (int kk = 0; kk < kmax; ++kk) kstep(kk);
     }
     if (kt + 1 < ktiles) store_tiles(buf ^ 1);
     __syncthreads();
