@@ -89,7 +89,9 @@ BGX_API int bgx_permute(const bgx_tensor *in, const bgx_tensor *out,
  * one final round-to-nearest-even to the storage type.
  * Axes: [0, n_par) are the output (parallel) axes in output order, then the
  * reduction axes (einsum.py:81).  c0 and out are dense row-major over the
- * parallel axes; c0 may equal out.  passthrough = (n_in == 1 && no reduction). */
+ * parallel axes; c0 may equal out or be NULL (zero initial output, i.e. +0.0 —
+ * what the reference computes from a zeros array).  passthrough = (n_in == 1
+ * && no reduction). */
 typedef struct {
   int32_t n_in;
   int32_t n_axes;

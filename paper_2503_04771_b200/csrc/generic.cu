@@ -38,23 +38,38 @@ template <typename S, typename T> __device__ __forceinline__ S st_as(T v) {
 template <> __device__ __forceinline__ float st_as<float, float>(float v) { return v; }
 template <> __device__ __forceinline__ double st_as<double, double>(double v) { return v; }
 
-template <typename S, typename T, int NIN>
+// DENSE: every input is laid out exactly like the (row-major) output over the
+// parallel axes and there is no reduction — the offsets are the output index.
+template <typename S, typename T, int NIN, bool DENSE>
 __global__ void __launch_bounds__(128)
 generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
   const int n_in = NIN > 0 ? NIN : d.n_in;
   const int n_par = d.n_par, n_axes = d.n_axes, n_red = n_axes - n_par;
   const bool passthrough = (n_in == 1 && n_red == 0);
+  const bool idx32 = n_out <= 0x7fffffffLL;
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n_out;
        o += (int64_t)gridDim.x * blockDim.x) {
     int64_t off[BGX_MAX_OPERANDS];
 #pragma unroll
-    for (int k = 0; k < BGX_MAX_OPERANDS; ++k) off[k] = 0;
-    int64_t rem = o;
-    for (int a = n_par - 1; a >= 0; --a) {
-      const int64_t e = d.extents[a];
-      const int64_t i = rem % e;
-      rem /= e;
-      for (int k = 0; k < n_in; ++k) off[k] += i * d.strides[k][a];
+    for (int k = 0; k < BGX_MAX_OPERANDS; ++k) off[k] = DENSE ? o : 0;
+    if (!DENSE) {
+      if (idx32) {   // 32-bit index arithmetic: the divisions dominate elementwise bodies
+        uint32_t rem = (uint32_t)o;
+        for (int a = n_par - 1; a >= 0; --a) {
+          const uint32_t e = (uint32_t)d.extents[a];
+          const uint32_t q = rem / e, i = rem - q * e;
+          rem = q;
+          for (int k = 0; k < n_in; ++k) off[k] += (int64_t)i * d.strides[k][a];
+        }
+      } else {
+        int64_t rem = o;
+        for (int a = n_par - 1; a >= 0; --a) {
+          const int64_t e = d.extents[a];
+          const int64_t i = rem % e;
+          rem /= e;
+          for (int k = 0; k < n_in; ++k) off[k] += i * d.strides[k][a];
+        }
+      }
     }
     const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
     S *out = static_cast<S *>(d.out);
@@ -62,7 +77,8 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
       out[o] = ins[0][off[0]];
       continue;
     }
-    T acc = ld_as<S, T>(static_cast<const S *>(d.c0) + o);
+    // c0 == NULL: zero initial output (+0.0, as the reference's zeros array)
+    T acc = d.c0 ? ld_as<S, T>(static_cast<const S *>(d.c0) + o) : T(0);
     if (red_points == 0) {
       out[o] = st_as<S, T>(acc);
       continue;
@@ -122,18 +138,35 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
   }
 }
 
+template <typename S, typename T, bool DENSE>
+void launch_generic_n(const bgx_generic_desc &d, int64_t n_out, int64_t red, unsigned blocks,
+                      cudaStream_t s) {
+  switch (d.n_in) {
+    case 1: generic_kernel<S, T, 1, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 2: generic_kernel<S, T, 2, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
+    case 3: generic_kernel<S, T, 3, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
+    default: generic_kernel<S, T, 0, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
+  }
+}
+
 template <typename S, typename T>
 int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
   const int sms = sm_count_current();
   if (sms <= 0) { set_error("bgx_generic: no device"); return BGX_ERR_NO_DEVICE; }
   int64_t blocks = (n_out + 127) / 128;
   if (blocks > (int64_t)sms * 64) blocks = (int64_t)sms * 64;
-  switch (d.n_in) {
-    case 1: generic_kernel<S, T, 1><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
-    case 2: generic_kernel<S, T, 2><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
-    case 3: generic_kernel<S, T, 3><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
-    default: generic_kernel<S, T, 0><<<(unsigned)blocks, 128, 0, s>>>(d, n_out, red); break;
+  // dense elementwise: no reduction and every input strided like the
+  // row-major output over the parallel axes
+  bool dense = d.n_axes == d.n_par;
+  for (int k = 0; k < d.n_in && dense; ++k) {
+    int64_t st = 1;
+    for (int a = d.n_par - 1; a >= 0 && dense; --a) {
+      if (d.extents[a] != 1 && d.strides[k][a] != st) dense = false;
+      st *= d.extents[a];
+    }
   }
+  if (dense) launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);
+  else launch_generic_n<S, T, false>(d, n_out, red, (unsigned)blocks, s);
   return check_launch("generic_kernel");
 }
 
@@ -158,8 +191,8 @@ extern "C" int bgx_generic(const bgx_generic_desc *d, void *stream) {
   }
   if (n_out == 0) return BGX_OK;
   BGX_CHECK_ARG(d->out != nullptr, "bgx_generic: null out");
+  // c0 == NULL means a zero initial output
   const bool passthrough = d->n_in == 1 && d->n_axes == d->n_par;
-  BGX_CHECK_ARG(passthrough || d->c0 != nullptr, "bgx_generic: null c0");
   if (red > 0 || passthrough)
     for (int k = 0; k < d->n_in; ++k) BGX_CHECK_ARG(d->ins[k] != nullptr, "bgx_generic: null input");
   cudaStream_t s = (cudaStream_t)stream;

@@ -126,12 +126,10 @@ def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
         for dim, name in enumerate(tup):
             d.strides[k][spec.axes.index(name)] = t.stride(dim)
     assert out.is_contiguous()
-    if c0 is None:
-        c0 = torch.zeros_like(out)
-    elif not c0.is_contiguous():
+    if c0 is not None and not c0.is_contiguous():
         c0 = permute(c0, torch.empty(c0.shape, dtype=c0.dtype, device=c0.device),
                      list(range(c0.dim())))
-    d.c0 = c0.data_ptr()
+    d.c0 = c0.data_ptr() if c0 is not None else None   # NULL: zero initial output
     d.out = out.data_ptr()
     with _on_device(out.device):
         _lib.check(lib.bgx_generic(d, _stream_ptr(out)), "bgx_generic")

@@ -78,13 +78,10 @@ class Prepared:
             for k, (t, tup) in enumerate(zip(ins, spec.inputs)):
                 for dim, name in enumerate(tup):
                     d.strides[k][spec.axes.index(name)] = t.stride(dim)
-            zeros = torch.zeros_like(out) if self.c0 is None else None
-            self._keep = zeros
-
             def run(xs, o, c0):
                 for k, t in enumerate(xs):
                     d.ins[k] = t.data_ptr()
-                d.c0 = (c0 if c0 is not None else zeros).data_ptr()
+                d.c0 = c0.data_ptr() if c0 is not None else None
                 d.out = o.data_ptr()
                 return self._lib.bgx_generic(d, torch.cuda.current_stream().cuda_stream)
             return run
