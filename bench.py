@@ -604,7 +604,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (torch.randn on device, bf16-rounded)",
-            "config": {"workload": WORKLOAD, "global_batch": I_, "parallelism": f"M-shard x{world}",
+            "config": {"workload": WORKLOAD, "I": I_, "K": K_, "J": J_, "L": L_,
+                       "parallelism": f"M-shard x{world}",
                        "order": "left-to-right (A@B)@C", "flop_per_step": CHAIN_FLOP,
                        "flop_min_order": CHAIN_FLOP_MINORDER,
                        "l2": "inputs exceed L2 (A 512 MiB, A@B 512 MiB per 1-GPU step)"},
