@@ -243,7 +243,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "parallelism": "host cores (OpenMP over outputs)",
+        "config": {"workload": WORKLOAD, "I": I_, "K": K_, "J": J_, "L": L_,
+                   "parallelism": "host cores (OpenMP over outputs)",
                    "step": f"{n} output elements of the reference loop nest, extrapolated"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                          "sample": f"{n} output elements per step x {args.steps} steps"},
