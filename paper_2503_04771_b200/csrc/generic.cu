@@ -16,6 +16,9 @@
 // rank-0 outputs) and for fp32 parity runs.
 #include "common.cuh"
 
+#include <stdlib.h>
+#include <type_traits>
+
 namespace bgx {
 namespace {
 
@@ -149,6 +152,152 @@ void launch_generic_n(const bgx_generic_desc &d, int64_t n_out, int64_t red, uns
   }
 }
 
+// ---- row reductions: one reduction axis, contiguous in every input ---------
+// (i,j)->(i), (i,j),(i,j)->(i), (i,j),(j)->(i) (GEMV), ...: each output is a
+// sequential chain over j (the reference order), so only the outputs give
+// parallelism.  The per-thread row walk of generic_kernel makes every warp
+// load touch 32 different rows; here a warp owns 32 consecutive outputs and
+// stages 32 x RT tiles of its 32 rows through shared memory with 4-byte
+// cp.async (each row segment is one coalesced 128-byte line), STAGES tiles in
+// flight; every lane then folds its own row from shared memory in order —
+// the same arithmetic sequence, bit-identical to the reference.
+constexpr int RR_TJ = 32;      // columns per tile
+constexpr int RR_STAGES = 4;   // tiles in flight per warp
+constexpr int RR_WARPS = 4;    // warps per block
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool pred) {
+  const int sz = pred ? 4 : 0;   // src-size 0: zero fill, no global access
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pred) {
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename T, int NIN>
+__global__ void __launch_bounds__(32 * RR_WARPS)
+rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) {
+  // shared_mask bit k: input k does not depend on the output index (e.g. the
+  // vector of a GEMV): its tile row is loaded once and read by every lane
+  // tile[stage][input][row][col], +1 column of padding against bank conflicts
+  extern __shared__ __align__(16) uint8_t rr_smem_raw[];
+  T *tiles = reinterpret_cast<T *>(rr_smem_raw);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int TSZ = 32 * (RR_TJ + 1);          // one tile
+  T *wtiles = tiles + (size_t)warp * RR_STAGES * NIN * TSZ;
+  const int n_par = d.n_par;
+  const int64_t E = d.extents[d.n_axes - 1];
+  const int64_t o0 = ((int64_t)blockIdx.x * RR_WARPS + warp) * 32;
+  if (o0 >= n_out) return;
+  const int64_t o = o0 + lane;
+  const bool row_ok = o < n_out;
+  // this lane's row bases
+  int64_t off[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) off[k] = 0;
+  if (row_ok) {
+    int64_t rem = o;
+    for (int a = n_par - 1; a >= 0; --a) {
+      const int64_t e = d.extents[a];
+      const int64_t i = rem % e;
+      rem /= e;
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) off[k] += i * d.strides[k][a];
+    }
+  }
+  const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+  const int64_t ntiles = (E + RR_TJ - 1) / RR_TJ;
+  auto issue = [&](int64_t t) {
+    const int stage = (int)(t % RR_STAGES);
+    const int64_t j = t * RR_TJ + lane;          // this lane's column of the tile
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      T *tile = wtiles + (stage * NIN + k) * TSZ;
+      auto copy_row = [&](int rr) {
+        const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
+        const bool ok = (o0 + rr < n_out) && j < E;
+        const T *src = ins[k] + (ok ? base + j : 0);
+        if constexpr (sizeof(T) == 4) cp_async4(tile + rr * (RR_TJ + 1) + lane, src, ok);
+        else cp_async8(tile + rr * (RR_TJ + 1) + lane, src, ok);
+      };
+      if ((shared_mask >> k) & 1) {
+        copy_row(0);
+      } else {
+        for (int rr = 0; rr < 32; ++rr) copy_row(rr);
+      }
+    }
+    cp_async_commit();
+  };
+  T acc = (row_ok && d.c0) ? static_cast<const T *>(d.c0)[o] : T(0);
+  for (int64_t t = 0; t < RR_STAGES - 1; ++t) {
+    if (t < ntiles) issue(t); else cp_async_commit();
+  }
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (t + RR_STAGES - 1 < ntiles) issue(t + RR_STAGES - 1); else cp_async_commit();
+    cp_async_wait<RR_STAGES - 1>();              // tile t has landed (this lane's copies)
+    __syncwarp();                                // ... and every lane's
+    const int stage = (int)(t % RR_STAGES);
+    const int jmax = (E - t * RR_TJ) < RR_TJ ? (int)(E - t * RR_TJ) : RR_TJ;
+    const T *row[NIN];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k)
+      row[k] = wtiles + (stage * NIN + k) * TSZ + (((shared_mask >> k) & 1) ? 0 : lane * (RR_TJ + 1));
+    if (jmax == RR_TJ) {
+#pragma unroll 8
+      for (int c = 0; c < RR_TJ; ++c) {
+        T p = row[0][c];
+#pragma unroll
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c]);
+        acc = add_rn<T>(p, acc);
+      }
+    } else {
+      for (int c = 0; c < jmax; ++c) {
+        T p = row[0][c];
+#pragma unroll
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c]);
+        acc = add_rn<T>(p, acc);
+      }
+    }
+    __syncwarp();                                // stage free before it is refilled
+  }
+  cp_async_wait<0>();
+  if (row_ok) static_cast<T *>(d.out)[o] = acc;
+}
+
+template <typename T>
+bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int *rc) {
+  if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2) return false;
+  const int ax = d.n_axes - 1;
+  for (int k = 0; k < d.n_in; ++k)
+    if (d.strides[k][ax] != 1) return false;
+  if (d.extents[ax] < 64 || n_out < 32) return false;
+  const int64_t blocks = (n_out + 32 * RR_WARPS - 1) / (32 * RR_WARPS);
+  if (blocks > 0x7fffffffLL) return false;
+  const size_t smem = (size_t)RR_WARPS * RR_STAGES * d.n_in * 32 * (RR_TJ + 1) * sizeof(T);
+  if (smem > 200 * 1024) return false;
+  uint32_t shared_mask = 0;
+  for (int k = 0; k < d.n_in; ++k) {
+    bool shared = true;
+    for (int a = 0; a < d.n_par; ++a) shared = shared && (d.strides[k][a] == 0 || d.extents[a] == 1);
+    if (shared) shared_mask |= 1u << k;
+  }
+  if (d.n_in == 1) {
+    cudaFuncSetAttribute(rowreduce_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rowreduce_kernel<T, 1><<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
+  } else {
+    cudaFuncSetAttribute(rowreduce_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rowreduce_kernel<T, 2><<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
+  }
+  *rc = check_launch("rowreduce_kernel");
+  return true;
+}
+
 template <typename S, typename T>
 int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
   const int sms = sm_count_current();
@@ -164,6 +313,12 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
       if (d.extents[a] != 1 && d.strides[k][a] != st) dense = false;
       st *= d.extents[a];
     }
+  }
+  if constexpr (std::is_same<S, T>::value) {   // f32 / f64 storage
+    int rc = 0;
+    // BGX_NO_ROWREDUCE=1: force the per-thread loop nest (A/B timing only)
+    static const bool no_rr = getenv("BGX_NO_ROWREDUCE") != nullptr;
+    if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
   }
   if (dense) launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);
   else launch_generic_n<S, T, false>(d, n_out, red, (unsigned)blocks, s);

@@ -193,12 +193,18 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
         return plan_chain(spec, ext, order=chain_order)
     groups = classify_two(spec, ext)
     if isinstance(groups, str):
-        if not ref_types:
-            raise NotImplementedError(f"{spec}: {groups} (no 16-bit generic kernel)")
         return GenericPlan(groups)
     batch, m, n, k = groups
     if ref_types and not k and (not m or not n):
         return GenericPlan("elementwise product (no reduction)")
+    if ref_types and mode in ("auto", "exact") and len(k) == 1 and (
+            _prod(ext[a] for a in m) == 1 or _prod(ext[a] for a in n) == 1):
+        # matrix-vector / batched row dots: one sequential chain per output
+        # along a contiguous axis is the row-reduction kernel's case (a GEMM
+        # tile would leave all but one row or column of every tile idle)
+        ka = k[0]
+        if all(st[tup.index(ka)] == 1 for tup, st in zip(spec.inputs, strides[:2])):
+            return GenericPlan("matrix-vector (row reductions)")
     return plan_gemm(spec, ext, strides, (batch, m, n, k), out_strides)
 
 

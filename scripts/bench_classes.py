@@ -30,6 +30,10 @@ def t(fn, iters=5):
 
 cases = [
     ("(i,j)->(i)", [(8192, 8192)]),
+    ("(i,j),(i,j)->(i)", [(8192, 8192), (8192, 8192)]),
+    ("(b,i,j)->(b,i)", [(64, 1024, 1024)]),
+    ("(i,j),(j)->(i)", [(8192, 8192), (8192,)]),
+    ("(i,j)->(i) f64", [(8192, 8192)]),
     ("(i,j)->(j)", [(8192, 8192)]),
     ("(i,j)->()", [(4096, 4096)]),
     ("(i,j),(i,j)->(i,j)", [(8192, 8192), (8192, 8192)]),
@@ -38,12 +42,14 @@ cases = [
     ("(i,j),(j,k),(k,l)->(i,l)", [(512, 512), (512, 512), (512, 512)]),
 ]
 for spec, shapes in cases:
-    xs = [torch.randn(s, device=dev) for s in shapes]
+    dt = torch.float64 if spec.endswith(" f64") else torch.float32
+    spec = spec.replace(" f64", "")
+    xs = [torch.randn(s, device=dev, dtype=dt) for s in shapes]
     executor.reset_launch_log()
     fn = lambda: contract(spec, *xs)  # noqa: E731
     ms = t(fn)
-    nbytes = sum(x.numel() * 4 for x in xs)
+    nbytes = sum(x.numel() * x.element_size() for x in xs)
     out = contract(spec, *xs)
-    nbytes += out.numel() * 4 * 2
+    nbytes += out.numel() * out.element_size()
     print(f"{spec:28s} {str(shapes):40s} {ms:9.3f} ms  {nbytes / ms / 1e6:8.1f} GB/s  "
           f"kernels={executor.launch_log()[:3]}", flush=True)

@@ -87,3 +87,38 @@ def test_clock_sample_one_cta_per_sm(dev):
     import bench
     c = bench.inband_clock(buf.cpu().numpy())
     assert c["inband_sms"] == n and 200 < c["sm_mhz_inband"] < 2500
+
+
+@pytest.mark.parametrize("text,shapes,dtype", [
+    ("(i,j)->(i)", [(1000, 3001)], np.float32),
+    ("(i,j)->(i)", [(37, 64)], np.float64),
+    ("(i,j),(i,j)->(i)", [(517, 1025), (517, 1025)], np.float32),
+    ("(i,j),(j)->(i)", [(300, 4097)], np.float32),
+    ("(b,i,j),(b,j)->(b,i)", [(3, 100, 777), (3, 777)], np.float64),
+    ("(b,i,j)->(b,i)", [(5, 64, 300)], np.float32),
+])
+def test_row_reduction_kernel_bit_exact(dev, text, shapes, dtype):
+    """Row reductions / matrix-vector bodies (one reduction axis, contiguous):
+    staged through shared memory by the row-reduction kernel, bit-identical to
+    the reference loop nest (oracle), with c0, ragged tiles and a broadcast
+    vector operand."""
+    spec = E.parse_einsum(text)
+    rng = np.random.default_rng(sum(sum(s) for s in shapes))
+    if text == "(i,j),(j)->(i)":
+        shapes = [shapes[0], (shapes[0][1],)]
+    arrs = [rng.standard_normal(s).astype(dtype) for s in shapes]
+    ext = {}
+    for a, tup in zip(arrs, spec.inputs):
+        ext.update(dict(zip(tup, a.shape)))
+    c0 = rng.standard_normal(tuple(ext[x] for x in spec.output)).astype(dtype)
+    got = contract(text, *[torch.from_numpy(a).to(dev) for a in arrs], c0=torch.from_numpy(c0).to(dev))
+    want = oracle.generic(list(spec.inputs), spec.output, arrs, c0)
+    uint = np.uint32 if dtype == np.float32 else np.uint64
+    assert np.array_equal(got.cpu().numpy().view(uint), np.asarray(want).view(uint)), text
+    # strided rows (a column slice): still one contiguous reduction axis per row
+    if text == "(i,j)->(i)" and dtype == np.float32:
+        big = torch.from_numpy(rng.standard_normal((1000, 4000)).astype(np.float32)).to(dev)
+        sl = big[:, 500:3501]
+        got2 = contract(text, sl)
+        want2 = oracle.generic([("i", "j")], ("i",), [sl.cpu().numpy()], np.zeros(1000, np.float32))
+        assert np.array_equal(got2.cpu().numpy().view(np.uint32), np.asarray(want2).view(np.uint32))
