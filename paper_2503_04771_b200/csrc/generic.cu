@@ -180,7 +180,10 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <typename T, int NIN>
+// COLS: the reduction axis is NOT contiguous but consecutive outputs are
+// (column sums, vector-matrix products): tile[step][lane] is then loaded
+// straight along the outputs — one coalesced line per reduction step.
+template <typename T, int NIN, bool COLS>
 __global__ void __launch_bounds__(32 * RR_WARPS)
 rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) {
   // shared_mask bit k: input k does not depend on the output index (e.g. the
@@ -219,17 +222,28 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
       T *tile = wtiles + (stage * NIN + k) * TSZ;
-      auto copy_row = [&](int rr) {
-        const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
-        const bool ok = (o0 + rr < n_out) && j < E;
-        const T *src = ins[k] + (ok ? base + j : 0);
-        if constexpr (sizeof(T) == 4) cp_async4(tile + rr * (RR_TJ + 1) + lane, src, ok);
-        else cp_async8(tile + rr * (RR_TJ + 1) + lane, src, ok);
-      };
-      if ((shared_mask >> k) & 1) {
-        copy_row(0);
+      if constexpr (COLS) {
+        const int64_t sk = d.strides[k][d.n_axes - 1];
+        for (int rr = 0; rr < 32; ++rr) {
+          const int64_t jj = t * RR_TJ + rr;       // reduction step of this tile row
+          const bool ok = row_ok && jj < E;
+          const T *src = ins[k] + (ok ? off[k] + jj * sk : 0);
+          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * (RR_TJ + 1) + lane, src, ok);
+          else cp_async8(tile + rr * (RR_TJ + 1) + lane, src, ok);
+        }
       } else {
-        for (int rr = 0; rr < 32; ++rr) copy_row(rr);
+        auto copy_row = [&](int rr) {
+          const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
+          const bool ok = (o0 + rr < n_out) && j < E;
+          const T *src = ins[k] + (ok ? base + j : 0);
+          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * (RR_TJ + 1) + lane, src, ok);
+          else cp_async8(tile + rr * (RR_TJ + 1) + lane, src, ok);
+        };
+        if ((shared_mask >> k) & 1) {
+          copy_row(0);
+        } else {
+          for (int rr = 0; rr < 32; ++rr) copy_row(rr);
+        }
       }
     }
     cp_async_commit();
@@ -244,23 +258,26 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     __syncwarp();                                // ... and every lane's
     const int stage = (int)(t % RR_STAGES);
     const int jmax = (E - t * RR_TJ) < RR_TJ ? (int)(E - t * RR_TJ) : RR_TJ;
+    // element c of this lane's chain: row layout tile[lane][c], column layout tile[c][lane]
     const T *row[NIN];
+    constexpr int CSTEP = COLS ? RR_TJ + 1 : 1;
 #pragma unroll
     for (int k = 0; k < NIN; ++k)
-      row[k] = wtiles + (stage * NIN + k) * TSZ + (((shared_mask >> k) & 1) ? 0 : lane * (RR_TJ + 1));
+      row[k] = wtiles + (stage * NIN + k) * TSZ +
+               (COLS ? lane : (((shared_mask >> k) & 1) ? 0 : lane * (RR_TJ + 1)));
     if (jmax == RR_TJ) {
 #pragma unroll 8
       for (int c = 0; c < RR_TJ; ++c) {
-        T p = row[0][c];
+        T p = row[0][c * CSTEP];
 #pragma unroll
-        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c]);
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * CSTEP]);
         acc = add_rn<T>(p, acc);
       }
     } else {
       for (int c = 0; c < jmax; ++c) {
-        T p = row[0][c];
+        T p = row[0][c * CSTEP];
 #pragma unroll
-        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c]);
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * CSTEP]);
         acc = add_rn<T>(p, acc);
       }
     }
@@ -272,11 +289,20 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
 
 template <typename T>
 bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int *rc) {
-  if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2) return false;
-  const int ax = d.n_axes - 1;
-  for (int k = 0; k < d.n_in; ++k)
-    if (d.strides[k][ax] != 1) return false;
+  if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2 || d.n_par < 1) return false;
+  const int ax = d.n_axes - 1, inner = d.n_par - 1;
+  bool rows = true, cols = true;
+  for (int k = 0; k < d.n_in; ++k) {
+    rows = rows && d.strides[k][ax] == 1;
+    // consecutive outputs at consecutive addresses (or the input ignores the
+    // output index entirely)
+    bool shared = true;
+    for (int a = 0; a < d.n_par; ++a) shared = shared && (d.strides[k][a] == 0 || d.extents[a] == 1);
+    cols = cols && (d.strides[k][inner] == 1 || shared);
+  }
+  if (!rows && !cols) return false;
   if (d.extents[ax] < 64 || n_out < 32) return false;
+  if (!rows && d.extents[inner] < 32) return false;   // warps would straddle short rows
   const int64_t blocks = (n_out + 32 * RR_WARPS - 1) / (32 * RR_WARPS);
   if (blocks > 0x7fffffffLL) return false;
   const size_t smem = (size_t)RR_WARPS * RR_STAGES * d.n_in * 32 * (RR_TJ + 1) * sizeof(T);
@@ -287,12 +313,14 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     for (int a = 0; a < d.n_par; ++a) shared = shared && (d.strides[k][a] == 0 || d.extents[a] == 1);
     if (shared) shared_mask |= 1u << k;
   }
-  if (d.n_in == 1) {
-    cudaFuncSetAttribute(rowreduce_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rowreduce_kernel<T, 1><<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
+  };
+  if (rows) {
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false>); else go(rowreduce_kernel<T, 2, false>);
   } else {
-    cudaFuncSetAttribute(rowreduce_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rowreduce_kernel<T, 2><<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, true>); else go(rowreduce_kernel<T, 2, true>);
   }
   *rc = check_launch("rowreduce_kernel");
   return true;

@@ -33,6 +33,8 @@ cases = [
     ("(i,j),(i,j)->(i)", [(8192, 8192), (8192, 8192)]),
     ("(b,i,j)->(b,i)", [(64, 1024, 1024)]),
     ("(i,j),(j)->(i)", [(8192, 8192), (8192,)]),
+    ("(i,j),(i)->(j)", [(8192, 8192), (8192,)]),
+    ("(b,i,j)->(b,j)", [(64, 1024, 1024)]),
     ("(i,j)->(i) f64", [(8192, 8192)]),
     ("(i,j)->(j)", [(8192, 8192)]),
     ("(i,j)->()", [(4096, 4096)]),

@@ -96,6 +96,11 @@ def test_clock_sample_one_cta_per_sm(dev):
     ("(i,j),(j)->(i)", [(300, 4097)], np.float32),
     ("(b,i,j),(b,j)->(b,i)", [(3, 100, 777), (3, 777)], np.float64),
     ("(b,i,j)->(b,i)", [(5, 64, 300)], np.float32),
+    ("(i,j)->(j)", [(3001, 1000)], np.float32),
+    ("(i,j)->(j)", [(64, 37)], np.float64),
+    ("(i,j),(i)->(j)", [(2049, 515), (2049,)], np.float32),
+    ("(b,i,j)->(b,j)", [(3, 700, 96)], np.float64),
+    ("(i,j),(i,j)->(j)", [(130, 100), (130, 100)], np.float32),
 ])
 def test_row_reduction_kernel_bit_exact(dev, text, shapes, dtype):
     """Row reductions / matrix-vector bodies (one reduction axis, contiguous):
@@ -106,6 +111,8 @@ def test_row_reduction_kernel_bit_exact(dev, text, shapes, dtype):
     rng = np.random.default_rng(sum(sum(s) for s in shapes))
     if text == "(i,j),(j)->(i)":
         shapes = [shapes[0], (shapes[0][1],)]
+    if text == "(i,j),(i)->(j)":
+        shapes = [shapes[0], (shapes[0][0],)]
     arrs = [rng.standard_normal(s).astype(dtype) for s in shapes]
     ext = {}
     for a, tup in zip(arrs, spec.inputs):
