@@ -326,6 +326,91 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   return true;
 }
 
+// ---- rank-0 outputs: ONE sequential chain (full reductions, dot products) ---
+// The reference order makes the whole reduction one dependent chain of adds;
+// only memory latency can be removed.  When every input is dense in the
+// reduction order (row-major over the reduction axes), the block's threads
+// stage the next tile of every input into shared memory (cp.async, coalesced)
+// while thread 0 folds the current one from shared memory — the fold runs at
+// the add latency instead of a global round trip per few elements.
+constexpr int CH_TILE = 4096;   // elements per input per stage
+constexpr int CH_THREADS = 256;
+
+template <typename T, int NIN>
+__global__ void __launch_bounds__(CH_THREADS) chain_kernel(const bgx_generic_desc d, int64_t total) {
+  extern __shared__ __align__(16) uint8_t ch_smem_raw[];
+  T *buf = reinterpret_cast<T *>(ch_smem_raw);     // [2][NIN][CH_TILE]
+  const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+  const int64_t ntiles = (total + CH_TILE - 1) / CH_TILE;
+  auto issue = [&](int64_t t) {
+    const int st = (int)(t & 1);
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      T *dst = buf + (st * NIN + k) * CH_TILE;
+      for (int e = threadIdx.x; e < CH_TILE; e += CH_THREADS) {
+        const int64_t g = t * CH_TILE + e;
+        const bool ok = g < total;
+        if constexpr (sizeof(T) == 4) cp_async4(dst + e, ins[k] + (ok ? g : 0), ok);
+        else cp_async8(dst + e, ins[k] + (ok ? g : 0), ok);
+      }
+    }
+    cp_async_commit();
+  };
+  T acc = d.c0 ? static_cast<const T *>(d.c0)[0] : T(0);
+  issue(0);
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) issue(t + 1); else cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int st = (int)(t & 1);
+      const int64_t n = total - t * CH_TILE < CH_TILE ? total - t * CH_TILE : CH_TILE;
+      const T *x0 = buf + (st * NIN + 0) * CH_TILE;
+      const T *x1 = NIN > 1 ? buf + (st * NIN + 1) * CH_TILE : nullptr;
+      int64_t e = 0;
+      if (n == CH_TILE) {
+        // unrolled: the shared loads run ahead of the dependent add chain
+#pragma unroll 16
+        for (; e < CH_TILE; ++e) {
+          T p = x0[e];
+          if constexpr (NIN > 1) p = mul_rn<T>(p, x1[e]);
+          acc = add_rn<T>(p, acc);
+        }
+      }
+      for (; e < n; ++e) {
+        T p = x0[e];
+        if constexpr (NIN > 1) p = mul_rn<T>(p, x1[e]);
+        acc = add_rn<T>(p, acc);
+      }
+    }
+    __syncthreads();                   // stage free before it is refilled
+  }
+  cp_async_wait<0>();
+  if (threadIdx.x == 0) static_cast<T *>(d.out)[0] = acc;
+}
+
+template <typename T>
+bool try_chain(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s, int *rc) {
+  if (n_out != 1 || d.n_par != 0 || d.n_in < 1 || d.n_in > 2 || red < 2 * CH_TILE) return false;
+  for (int k = 0; k < d.n_in; ++k) {   // dense in the reduction order
+    int64_t st = 1;
+    for (int a = d.n_axes - 1; a >= 0; --a) {
+      if (d.extents[a] != 1 && d.strides[k][a] != st) return false;
+      st *= d.extents[a];
+    }
+  }
+  const size_t smem = (size_t)2 * d.n_in * CH_TILE * sizeof(T);
+  if (d.n_in == 1) {
+    cudaFuncSetAttribute(chain_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    chain_kernel<T, 1><<<1, CH_THREADS, smem, s>>>(d, red);
+  } else {
+    cudaFuncSetAttribute(chain_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    chain_kernel<T, 2><<<1, CH_THREADS, smem, s>>>(d, red);
+  }
+  *rc = check_launch("chain_kernel");
+  return true;
+}
+
 template <typename S, typename T>
 int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
   const int sms = sm_count_current();
@@ -347,6 +432,7 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
     // BGX_NO_ROWREDUCE=1: force the per-thread loop nest (A/B timing only)
     static const bool no_rr = getenv("BGX_NO_ROWREDUCE") != nullptr;
     if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
+    if (!no_rr && try_chain<T>(d, n_out, red, s, &rc)) return rc;
   }
   if (dense) launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);
   else launch_generic_n<S, T, false>(d, n_out, red, (unsigned)blocks, s);

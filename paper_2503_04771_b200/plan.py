@@ -197,6 +197,10 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
     batch, m, n, k = groups
     if ref_types and not k and (not m or not n):
         return GenericPlan("elementwise product (no reduction)")
+    if ref_types and mode in ("auto", "exact") and not batch and k and \
+            _prod(ext[a] for a in m) == 1 and _prod(ext[a] for a in n) == 1:
+        # a full dot product: one sequential chain (the chain kernel's case)
+        return GenericPlan("dot product (one chain)")
     if ref_types and mode in ("auto", "exact") and len(k) == 1 and (
             _prod(ext[a] for a in m) == 1 or _prod(ext[a] for a in n) == 1):
         # matrix-vector / batched row dots: one sequential chain per output

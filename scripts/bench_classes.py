@@ -38,6 +38,7 @@ cases = [
     ("(i,j)->(i) f64", [(8192, 8192)]),
     ("(i,j)->(j)", [(8192, 8192)]),
     ("(i,j)->()", [(4096, 4096)]),
+    ("(i,j),(i,j)->()", [(2048, 2048), (2048, 2048)]),
     ("(i,j),(i,j)->(i,j)", [(8192, 8192), (8192, 8192)]),
     ("(i),(j)->(i,j)", [(8192,), (8192,)]),
     ("(b,i,j),(b,j)->(b,i)", [(64, 1024, 1024), (64, 1024)]),

@@ -101,6 +101,8 @@ def test_clock_sample_one_cta_per_sm(dev):
     ("(i,j),(i)->(j)", [(2049, 515), (2049,)], np.float32),
     ("(b,i,j)->(b,j)", [(3, 700, 96)], np.float64),
     ("(i,j),(i,j)->(j)", [(130, 100), (130, 100)], np.float32),
+    ("(i,j)->()", [(300, 301)], np.float32),
+    ("(i,j),(i,j)->()", [(129, 257), (129, 257)], np.float64),
 ])
 def test_row_reduction_kernel_bit_exact(dev, text, shapes, dtype):
     """Row reductions / matrix-vector bodies (one reduction axis, contiguous):
