@@ -594,6 +594,25 @@ def main():
         if not args.no_cpu:
             cpu = cpu_baseline(A[:1].float().cpu().numpy(), B.float().cpu().numpy(),
                                C.float().cpu().numpy())
+    # the tile shape the library picked for the chain GEMMs (transparency)
+    tile_info = None
+    try:
+        d = _lib.BgxContractDesc()
+        d.batch, d.M, d.N, d.K = 1, rows, J_, K_
+        d.a_stride[:] = [0, K_, 1]
+        d.b_stride[:] = [0, J_, 1]
+        d.o_stride[:] = [0, J_, 1]
+        d.in_dtype = d.out_dtype = _lib.BF16
+        d.mode = _lib.MODE_TC
+        d.a, d.b, d.out = A.data_ptr(), B.data_ptr(), T.data_ptr()
+        cg, bn = _lib._i32(), _lib._i32()
+        sp, ws = _lib._i32(), _lib._i64()
+        _lib.load().bgx_contract_tile(d, cg, bn)
+        _lib.load().bgx_contract_splitk_plan(d, sp, ws)
+        tile_info = {"cta_group": cg.value, "tile_m": 128 * cg.value, "tile_n": bn.value,
+                     "splits": sp.value}
+    except Exception:  # noqa: BLE001
+        pass
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tpath):
@@ -614,6 +633,7 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"],
                          "unit": "TFLOP/s", "frac": achieved / pk["bf16"], "traffic": traffic,
                          "kernel": "tc_gemm_kernel (tcgen05/TMEM/TMA)",
+                         "tile": tile_info,
                          "flop_per_launch": gemm_flop, "launch_ms": gemm_ms,
                          "peak_source": pk["source"] + " burst bf16",
                          "frac_of_sustained": achieved / pk["bf16_sustained"]},
