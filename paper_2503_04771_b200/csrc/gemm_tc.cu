@@ -591,6 +591,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         }
         tmem_ld_wait();
         arrive_empty(acc);
+        // a CTA half entirely below the last output row has no owner (its
+        // rows do not exist): nothing to deliver, no counter to bump
+        if (tm * C::TILE_M + rank * BM >= p.M) continue;
         constexpr int NT = 32 * EPI_WARPS;
         // (2) local split-K: the last slice of this tile sums the slices in
         //     slice order and forwards the rank's partial to the owner

@@ -84,16 +84,37 @@ def ksplit_reduce(partial: torch.Tensor, *, c0: torch.Tensor | None = None, out_
     return fn(red.contiguous(), out, c0_local.contiguous() if c0_local is not None else None)
 
 
+_FUSED_CACHE: dict = {}
+
+
 def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
                     c0: torch.Tensor | None = None, out_dtype=None, group=None,
-                    scatter: bool = False) -> torch.Tensor:
+                    scatter: bool = False, fused: bool = False) -> torch.Tensor:
     """K-split 2-operand contraction.  ``a_slab``/``b_slab`` hold this rank's
     K range (``k_range``) of the reduction index of ``spec``.  The local
     partial is a tcgen05 (or SIMT) contraction with f32 output; the partials
     are then combined by ``ksplit_reduce`` (one NCCL collective).  Returns the
-    full output on every rank, or this rank's row slab with ``scatter``."""
+    full output on every rank, or this rank's row slab with ``scatter``.
+    ``fused=True`` (with ``scatter``) runs the GEMM and the reduce-scatter as
+    one kernel (``FusedKSplit``, cached per shape/dtype/group); the returned
+    slab is then ``owned_rows`` of the output (rows per owner rounded to 128)."""
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
+    if fused:
+        if not scatter:
+            raise ValueError("fused K-split returns this rank's row slab: pass scatter=True")
+        key = (spec, tuple(a_slab.shape), tuple(a_slab.stride()), tuple(b_slab.shape),
+               tuple(b_slab.stride()), a_slab.dtype, out_dtype, id(group), c0 is not None,
+               a_slab.device)
+        f = _FUSED_CACHE.get(key)
+        if f is None:
+            f = _FUSED_CACHE[key] = FusedKSplit(spec, a_slab, b_slab, out_dtype=out_dtype,
+                                                group=group, with_c0=c0 is not None)
+        c0_local = None
+        if c0 is not None:
+            lo, hi = owned_rows(f.M, f.plan.rows_per_owner, f.rank)
+            c0_local = c0[lo:hi]
+        return f(a_slab, b_slab, c0=c0_local)
     partial = contract(spec, a_slab, b_slab, out_dtype=torch.float32)
     return ksplit_reduce(partial, c0=c0, out_dtype=out_dtype or a_slab.dtype, group=group,
                          scatter=scatter)

@@ -27,7 +27,8 @@ def _slabs(a, b, world, ks=None):
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-@pytest.mark.parametrize("M,N,K", [(1024, 1024, 16384), (4096, 512, 8192), (1000, 1000, 4096)])
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 16384), (4096, 512, 8192), (1000, 1000, 4096),
+                                   (384, 256, 8192), (200, 512, 4096)])
 def test_emulated_reduce_scatter_matches(dev, world, M, N, K):
     g = torch.Generator(device=dev).manual_seed(M + N + world)
     a = torch.randn(M, K, device=dev, generator=g).bfloat16()
@@ -114,3 +115,14 @@ def test_fused_symmetric_memory_world1(dev):
         assert _relf(y, a.double() @ b.double() + c0.double()) < 1e-2
     finally:
         dist.destroy_process_group()
+
+
+def test_ksplit_contract_fused_flag_single_rank(dev):
+    a = torch.randn(384, 8192, device=dev).bfloat16()
+    b = torch.randn(8192, 256, device=dev).bfloat16()
+    y = shard.ksplit_contract(MM, a, b, scatter=True, fused=True)
+    assert _relf(y, a.double() @ b.double()) < 1e-2
+    y2 = shard.ksplit_contract(MM, a, b, scatter=True, fused=True)   # cached object
+    assert torch.equal(y.view(torch.int16), y2.view(torch.int16))
+    with pytest.raises(ValueError, match="scatter=True"):
+        shard.ksplit_contract(MM, a, b, fused=True)
