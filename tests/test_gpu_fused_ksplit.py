@@ -126,3 +126,15 @@ def test_ksplit_contract_fused_flag_single_rank(dev):
     assert torch.equal(y.view(torch.int16), y2.view(torch.int16))
     with pytest.raises(ValueError, match="scatter=True"):
         shard.ksplit_contract(MM, a, b, fused=True)
+
+
+@pytest.mark.parametrize("M,world", [(300, 4), (130, 2), (129, 8), (640, 3)])
+def test_emulated_ragged_owners(dev, M, world):
+    """Owners with partial or no rows (rows_per_owner rounded to 128)."""
+    N, K = 384, 2048 * world
+    a = torch.randn(M, K, device=dev).bfloat16()
+    b = torch.randn(K, N, device=dev).bfloat16()
+    A, B = _slabs(a, b, world)
+    out = shard.emulate_fused_ksplit(MM, A, B, out_dtype=torch.float32)
+    assert out.shape == (M, N)
+    assert _relf(out, a.double() @ b.double()) < 1e-5
