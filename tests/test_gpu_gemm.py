@@ -378,3 +378,34 @@ def test_cluster_n2_with_uniform_splitk(dev):
     y = contract("(i,k),(k,j)->(i,j)", a, b, out_dtype=torch.float32, schedule=dict(sc, cluster_n=2))
     assert executor.launch_log() == ["tcgen05-splitk"]
     assert torch.equal(y, base)
+
+
+def test_gemm_fuzz_shapes_layouts_schedules(dev):
+    """Randomised shapes (ragged M/N/K, batch), operand majorness, output
+    dtype, c0 and schedules (tile, CTA pair, A-multicast clusters, split-K,
+    tail split) against an f64 product: relF <= 1e-2, and no device fault."""
+    import random
+    r = random.Random(4711)
+    scheds = [None, {"tile_n": 128, "cta_group": 1}, {"tile_n": 256, "cta_group": 2},
+              {"tile_n": 512, "cta_group": 2}, {"cta_group": 2, "tile_n": 256, "cluster_n": 2},
+              {"splits": 3}, {"splits": -2}, {"tile_n": 64, "cta_group": 1, "raster": -4}]
+    for it in range(200):
+        bt = r.choice([1, 1, 1, 3])
+        M = r.randint(1, 1500)
+        N = 8 * r.randint(1, 300) if r.random() < 0.8 else r.randint(1, 2400)
+        K = r.choice([8, 64, 200, 1000, 4104]) if r.random() < 0.8 else r.randint(1, 5000)
+        dt = r.choice([torch.bfloat16, torch.float16])
+        a = torch.randn(bt, M, K, device=dev).to(dt)
+        b = torch.randn(bt, K, N, device=dev).to(dt)
+        if r.random() < 0.3:
+            a = a.transpose(1, 2).contiguous().transpose(1, 2)
+        if r.random() < 0.3:
+            b = b.transpose(1, 2).contiguous().transpose(1, 2)
+        out_dt = r.choice([dt, torch.float32])
+        c0 = torch.randn(bt, M, N, device=dev).to(out_dt) if r.random() < 0.3 else None
+        sc = r.choice(scheds)
+        y = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b, c0=c0, out_dtype=out_dt, schedule=sc)
+        torch.cuda.synchronize()
+        want = a.double() @ b.double() + (c0.double() if c0 is not None else 0)
+        err = float((y.double() - want).norm() / want.norm())
+        assert err <= 1e-2, (it, bt, M, N, K, dt, out_dt, sc, err)
