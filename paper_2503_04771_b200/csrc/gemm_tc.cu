@@ -1283,8 +1283,9 @@ int tc_rs_plan(const bgx_contract_desc &d, int world, bgx_rs_plan *pl) {
   const int64_t rows = (d.M + world - 1) / world;
   // CTA pairs (256-row tiles); ownership is per CTA (128 rows), so each
   // owner's slab only has to be a multiple of 128 rows
-  const int cg = d.M > 128 ? 2 : 1;
+  // instantiated fused variants: (1, 128), (1, 256), (2, 256)
   const int bn = d.N > 128 ? 256 : 128;
+  const int cg = (d.M > 128 && bn == 256) ? 2 : 1;
   const int64_t tile_m = 128 * cg;
   pl->cta_group = cg;
   pl->tile_n = bn;

@@ -138,3 +138,24 @@ def test_emulated_ragged_owners(dev, M, world):
     out = shard.emulate_fused_ksplit(MM, A, B, out_dtype=torch.float32)
     assert out.shape == (M, N)
     assert _relf(out, a.double() @ b.double()) < 1e-5
+
+
+def test_fused_reduce_scatter_fuzz(dev):
+    """Random world sizes, ragged M, N, uneven K slabs, c0 and output dtype."""
+    import random
+    r = random.Random(99)
+    for it in range(25):
+        world = r.randint(1, 8)
+        M = r.randint(1, 1200)
+        N = 8 * r.randint(1, 160)
+        ks = sorted(r.sample(range(8, 8 * 900, 8), world - 1)) if world > 1 else []
+        bounds = list(zip([0] + ks, ks + [8 * 900]))
+        a = torch.randn(M, 8 * 900, device=dev).bfloat16()
+        b = torch.randn(8 * 900, N, device=dev).bfloat16()
+        out_dt = r.choice([torch.bfloat16, torch.float32])
+        c0 = torch.randn(M, N, device=dev).to(out_dt) if r.random() < 0.5 else None
+        A, B = _slabs(a, b, world, bounds)
+        y = shard.emulate_fused_ksplit(MM, A, B, c0=c0, out_dtype=out_dt)
+        torch.cuda.synchronize()
+        want = a.double() @ b.double() + (c0.double() if c0 is not None else 0)
+        assert _relf(y, want) < 1e-2, (it, world, M, N, out_dt)
