@@ -47,3 +47,27 @@ def test_prepared_fast_path_and_errors(dev):
     assert executor.launch_log() == []      # no executor round trip
     with pytest.raises(ValueError, match="different shapes"):
         p(torch.randn(64, 64, device=dev).bfloat16(), b)
+
+
+def test_prepared_fuzz_matches_contract(dev):
+    """prepare() (pre-built descriptors, pointer patching) and its CUDA-graph
+    form give exactly what contract() gives, over random specs, dtypes and
+    strided views."""
+    import random
+    from paper_2503_04771_b200 import contract, prepare
+    r = random.Random(5)
+    specs = ["(i,k),(k,j)->(i,j)", "(b,i,k),(b,k,j)->(b,i,j)", "(i,j)->(j,i)", "(i,j)->(i)",
+             "(i,j),(i,j)->(i,j)", "(i,k),(j,k)->(i,j)", "(i,j,k)->(k,i,j)"]
+    for it in range(30):
+        text = r.choice(specs)
+        dt = r.choice([torch.float32, torch.bfloat16])
+        spec_ins = [t.split(",") for t in text.split("->")[0][1:-1].split("),(")]
+        ext = {a: 8 * r.randint(1, 40) for t in spec_ins for a in t}
+        xs = [torch.randn([ext[a] for a in t], device=dev).to(dt) for t in spec_ins]
+        if r.random() < 0.3 and xs[0].dim() >= 2:
+            xs[0] = xs[0].transpose(0, 1).contiguous().transpose(0, 1)
+        want = contract(text, *xs)
+        p = prepare(text, *xs)
+        assert torch.equal(p(*xs), want), text
+        g = prepare(text, *xs, graph=True)
+        assert torch.equal(g(), want), text
