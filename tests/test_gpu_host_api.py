@@ -57,3 +57,25 @@ def test_contract_devices_matches_single_device(dev):
         assert torch.equal(sh, whole)
     with pytest.raises(ValueError, match="leading index"):
         contract("(k,i),(k,j)->(i,j)", a.t(), b, devices=[0, 0])
+
+
+def test_contract_host_fuzz(dev):
+    """contract_host over random row counts around the chunk size, with and
+    without c0 / pinned buffers: identical to contract() on the device."""
+    import random
+    r = random.Random(12)
+    for it in range(12):
+        rows = r.choice([1, 100, 2047, 2048, 2049, 5000])
+        K, N = 8 * r.randint(1, 64), 8 * r.randint(1, 64)
+        pinned = r.random() < 0.8
+        a = torch.randn(rows, K).bfloat16()
+        b = torch.randn(K, N).bfloat16()
+        c0 = torch.randn(rows, N).bfloat16() if r.random() < 0.4 else None
+        if pinned:
+            a, b = a.pin_memory(), b.pin_memory()
+            c0 = c0.pin_memory() if c0 is not None else None
+        got = contract_host("(i,k),(k,j)->(i,j)", a, b, c0=c0, device=dev,
+                            chunk_rows=r.choice([None, 512, 2048]))
+        want = contract("(i,k),(k,j)->(i,j)", a.to(dev), b.to(dev),
+                        c0=c0.to(dev) if c0 is not None else None)
+        assert torch.equal(got, want.cpu()), (it, rows, K, N, pinned)
