@@ -100,8 +100,11 @@ def contract_host(spec, *host_operands: torch.Tensor, out: torch.Tensor | None =
     buffers are pinned, the work is pipelined over row chunks on three
     streams: H2D of chunk i+1 and D2H of chunk i-1 overlap the contraction of
     chunk i (PCIe is full duplex), so the call costs ~max(H2D, compute, D2H)
-    instead of their sum.  Results are identical to the unchunked call (row
-    slabs are independent; every kernel's per-row arithmetic is unchanged)."""
+    instead of their sum.  Row slabs are independent, so each chunk computes
+    exactly its rows of the unchunked result — bit for bit, unless the tile
+    planner splits K differently for the chunk than for the whole (long K:
+    split-K / tail split), which reorders the f32 summation (relative
+    difference ~1e-7)."""
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
     device = torch.device(device) if device is not None else torch.device(
