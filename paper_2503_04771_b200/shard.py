@@ -320,8 +320,9 @@ def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> 
     device contracts its slab on its own current stream — launches are
     asynchronous, so the devices run concurrently — and the slabs are copied
     back into ``out`` on the operands' device.  No collective: the slabs are
-    independent (the §8e M-shard), so the result equals the single-device one
-    row for row."""
+    independent (the §8e M-shard), so every row is computed as on one device —
+    bit for bit unless the planner splits K differently for a slab (long K),
+    which only reorders the f32 summation."""
     from .api import _row_streamable, output_shape
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
