@@ -222,7 +222,16 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
       T *tile = wtiles + (stage * NIN + k) * TSZ;
-      if constexpr (COLS) {
+      if (COLS && ((shared_mask >> k) & 1)) {
+        // shared operand (e.g. the vector of a vector-matrix product): one
+        // element per reduction step, lane l loads step l of the tile
+        const int64_t sk = d.strides[k][d.n_axes - 1];
+        const int64_t jj = t * RR_TJ + lane;
+        const bool ok = jj < E;
+        const T *src = ins[k] + (ok ? off[k] + jj * sk : 0);
+        if constexpr (sizeof(T) == 4) cp_async4(tile + lane, src, ok);
+        else cp_async8(tile + lane, src, ok);
+      } else if constexpr (COLS) {
         const int64_t sk = d.strides[k][d.n_axes - 1];
         for (int rr = 0; rr < 32; ++rr) {
           const int64_t jj = t * RR_TJ + rr;       // reduction step of this tile row
@@ -260,24 +269,26 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     const int jmax = (E - t * RR_TJ) < RR_TJ ? (int)(E - t * RR_TJ) : RR_TJ;
     // element c of this lane's chain: row layout tile[lane][c], column layout tile[c][lane]
     const T *row[NIN];
-    constexpr int CSTEP = COLS ? RR_TJ + 1 : 1;
+    int cstep[NIN];
 #pragma unroll
-    for (int k = 0; k < NIN; ++k)
-      row[k] = wtiles + (stage * NIN + k) * TSZ +
-               (COLS ? lane : (((shared_mask >> k) & 1) ? 0 : lane * (RR_TJ + 1)));
+    for (int k = 0; k < NIN; ++k) {
+      const bool sh = (shared_mask >> k) & 1;
+      row[k] = wtiles + (stage * NIN + k) * TSZ + (sh ? 0 : (COLS ? lane : lane * (RR_TJ + 1)));
+      cstep[k] = (COLS && !sh) ? RR_TJ + 1 : 1;
+    }
     if (jmax == RR_TJ) {
 #pragma unroll 8
       for (int c = 0; c < RR_TJ; ++c) {
-        T p = row[0][c * CSTEP];
+        T p = row[0][c * cstep[0]];
 #pragma unroll
-        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * CSTEP]);
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * cstep[k]]);
         acc = add_rn<T>(p, acc);
       }
     } else {
       for (int c = 0; c < jmax; ++c) {
-        T p = row[0][c * CSTEP];
+        T p = row[0][c * cstep[0]];
 #pragma unroll
-        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * CSTEP]);
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * cstep[k]]);
         acc = add_rn<T>(p, acc);
       }
     }

@@ -207,10 +207,13 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
         # along a contiguous axis is the row-reduction kernel's case (a GEMM
         # tile would leave all but one row or column of every tile idle)
         ka = k[0]
-        # (vector-matrix products with a strided reduction axis stay on the
-        # SIMT GEMM: measured 2x faster than the column-staged reduction)
-        if all(st[tup.index(ka)] == 1 for tup, st in zip(spec.inputs, strides[:2])):
-            return GenericPlan("matrix-vector (row reductions)")
+        pairs = list(zip(spec.inputs, strides[:2]))
+        rows_ok = all(st[tup.index(ka)] == 1 for tup, st in pairs)
+        inner = spec.output[-1] if spec.output else None
+        cols_ok = inner is not None and ext[inner] >= 32 and all(
+            inner not in tup or st[tup.index(inner)] == 1 for tup, st in pairs)
+        if rows_ok or cols_ok:
+            return GenericPlan("matrix-vector (row / column reductions)")
     return plan_gemm(spec, ext, strides, (batch, m, n, k), out_strides)
 
 
