@@ -177,6 +177,13 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
                 setattr(d.sched, k, int(v))
     kind = lib.bgx_contract_kernel(d)
     _lib.check(kind if kind < 0 else 0, "bgx_contract_kernel")
+    if (kind == _lib.KERNEL_SIMT16 and mode == "auto" and a is not None and b is not None
+            and 2 * batch * M * N * K >= PAD_MIN_FLOP):
+        # 16-bit operands whose strides/extents are not TMA-legal (odd K or N,
+        # unaligned views): stage zero-padded, aligned copies and run on the
+        # tensor cores instead of the CUDA-core fallback (~40x slower at scale)
+        return _contract_padded(a, a_strides, b, b_strides, out, o_strides, batch=batch, M=M,
+                                N=N, K=K, c0=c0, c_strides=c_strides, schedule=schedule)
     splits = _lib._i32(1)
     ws_bytes = _lib._i64(0)
     if kind == _lib.KERNEL_TC and not (schedule and schedule.get("no_splitk")):
@@ -200,6 +207,38 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
             return kind
         _lib.check(lib.bgx_contract(d, _stream_ptr(out)), "bgx_contract")
     _log(_lib.KERNEL_NAMES.get(kind, "contract"))
+    return kind
+
+
+PAD_MIN_FLOP = 1 << 28
+
+
+def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0,
+                     c_strides, schedule) -> int:
+    """K and N rounded up to multiples of 8 with zero padding (zero products
+    leave every sum unchanged), operands copied by bgx_permute into aligned
+    dense buffers, one tcgen05 contraction, valid columns copied back."""
+    dev = out.device
+    kp, np_ = (K + 7) // 8 * 8, (N + 7) // 8 * 8
+    av = torch.as_strided(a, (batch, M, K), a_strides, a.storage_offset())
+    bv = torch.as_strided(b, (batch, K, N), b_strides, b.storage_offset())
+    ap = torch.zeros((batch, M, kp), dtype=a.dtype, device=dev)
+    bp = torch.zeros((batch, kp, np_), dtype=b.dtype, device=dev)
+    permute(av, ap[:, :, :K], (0, 1, 2))
+    permute(bv, bp[:, :K, :N], (0, 1, 2))
+    cp = None
+    cs = (0, 0, 0)
+    if c0 is not None:
+        cv = torch.as_strided(c0, (batch, M, N), c_strides, c0.storage_offset())
+        cp = torch.zeros((batch, M, np_), dtype=c0.dtype, device=dev)
+        permute(cv, cp[:, :, :N], (0, 1, 2))
+        cs = (M * np_, np_, 1)
+    op = torch.empty((batch, M, np_), dtype=out.dtype, device=dev)
+    kind = contract_raw(ap, (M * kp, kp, 1), bp, (kp * np_, np_, 1), op, (M * np_, np_, 1),
+                        batch=batch, M=M, N=np_, K=kp, c0=cp, c_strides=cs, mode="auto",
+                        schedule=schedule)
+    ov = torch.as_strided(out, (batch, M, N), o_strides, out.storage_offset())
+    permute(op[:, :, :N], ov, (0, 1, 2))
     return kind
 
 

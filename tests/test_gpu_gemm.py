@@ -409,3 +409,23 @@ def test_gemm_fuzz_shapes_layouts_schedules(dev):
         want = a.double() @ b.double() + (c0.double() if c0 is not None else 0)
         err = float((y.double() - want).norm() / want.norm())
         assert err <= 1e-2, (it, bt, M, N, K, dt, out_dt, sc, err)
+
+
+@pytest.mark.parametrize("M,N,K,with_c0", [(2048, 1001, 999, False), (1500, 4095, 2049, True),
+                                           (3000, 640, 1003, True)])
+def test_unaligned_16bit_gemm_padded_onto_tensor_cores(dev, M, N, K, with_c0):
+    """16-bit GEMMs with odd K / N (not TMA-legal) are zero-padded onto the
+    tensor cores instead of the CUDA-core fallback: tolerance vs f64, and
+    the launch log shows tcgen05."""
+    a = torch.randn(M, K, device=dev).bfloat16()
+    b = torch.randn(K, N, device=dev).bfloat16()
+    c0 = torch.randn(M, N, device=dev).bfloat16() if with_c0 else None
+    executor.reset_launch_log()
+    y = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0)
+    assert any(k.startswith("tcgen05") for k in executor.launch_log()), executor.launch_log()
+    want = a.double() @ b.double() + (c0.double() if c0 is not None else 0)
+    assert float((y.double() - want).norm() / want.norm()) <= 1e-2
+    # strided output view
+    big = torch.zeros(M, N + 5, device=dev, dtype=torch.bfloat16)
+    contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, out=big[:, 2:N + 2])
+    assert torch.equal(big[:, 2:N + 2], y)
