@@ -1,0 +1,44 @@
+"""Performance floors (generous, power-cap tolerant) so that a regression in
+a later change shows up in `pytest -m gpu`, not only in bench.py: the
+headline GEMM shape, BASELINE config 4, and the config-2 permutation."""
+
+import statistics
+
+import pytest
+import torch
+
+from paper_2503_04771_b200.api import contract
+
+pytestmark = pytest.mark.gpu
+
+
+def _ms(fn, iters=5):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(iters)]
+    for s, e in ev:
+        s.record()
+        fn()
+        e.record()
+    torch.cuda.synchronize()
+    return statistics.median(s.elapsed_time(e) for s, e in ev)
+
+
+@pytest.mark.parametrize("M,N,K,floor", [(16384, 8192, 8192, 1100.0), (4096, 4096, 4096, 1000.0)])
+def test_gemm_floor(dev, M, N, K, floor):
+    a = torch.randn(M, K, device=dev).bfloat16()
+    b = torch.randn(K, N, device=dev).bfloat16()
+    out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    ms = _ms(lambda: contract("(i,k),(k,j)->(i,j)", a, b, out=out))
+    tflops = 2 * M * N * K / ms / 1e9
+    assert tflops >= floor, f"{M}x{N}x{K}: {tflops:.0f} TFLOP/s < {floor}"
+
+
+def test_permute_floor(dev):
+    x = torch.randn(8192, 8192, device=dev)
+    out = torch.empty(8192, 8192, device=dev)
+    ms = _ms(lambda: contract("(i,j)->(j,i)", x, out=out))
+    gbs = 2 * x.numel() * 4 / ms / 1e6
+    assert gbs >= 4000.0, f"transpose {gbs:.0f} GB/s < 4000"
