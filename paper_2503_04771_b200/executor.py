@@ -176,14 +176,20 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
             else:
                 setattr(d.sched, k, int(v))
     kind = lib.bgx_contract_kernel(d)
-    _lib.check(kind if kind < 0 else 0, "bgx_contract_kernel")
-    if (kind == _lib.KERNEL_SIMT16 and mode == "auto" and a is not None and b is not None
-            and 2 * batch * M * N * K >= PAD_MIN_FLOP):
-        # 16-bit operands whose strides/extents are not TMA-legal (odd K or N,
+    pad_ok = a is not None and b is not None and not getattr(contract_raw, "_in_pad", False)
+    if pad_ok and ((kind == _lib.KERNEL_SIMT16 and mode == "auto"
+                    and 2 * batch * M * N * K >= PAD_MIN_FLOP)
+                   or (kind == _lib.ERR_UNSUPPORTED and mode in ("tc", "tf32")
+                       and in_dtype is None and a.dtype in (torch.bfloat16, torch.float16,
+                                                            torch.float32))):
+        # operands whose strides/extents are not TMA-legal (odd K or N,
         # unaligned views): stage zero-padded, aligned copies and run on the
         # tensor cores instead of the CUDA-core fallback (~40x slower at scale)
+        # or, in the tensor-core-only modes, instead of failing
         return _contract_padded(a, a_strides, b, b_strides, out, o_strides, batch=batch, M=M,
-                                N=N, K=K, c0=c0, c_strides=c_strides, schedule=schedule)
+                                N=N, K=K, c0=c0, c_strides=c_strides, schedule=schedule,
+                                mode=mode)
+    _lib.check(kind if kind < 0 else 0, "bgx_contract_kernel")
     splits = _lib._i32(1)
     ws_bytes = _lib._i64(0)
     if kind == _lib.KERNEL_TC and not (schedule and schedule.get("no_splitk")):
@@ -214,12 +220,13 @@ PAD_MIN_FLOP = 1 << 28
 
 
 def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0,
-                     c_strides, schedule) -> int:
-    """K and N rounded up to multiples of 8 with zero padding (zero products
-    leave every sum unchanged), operands copied by bgx_permute into aligned
-    dense buffers, one tcgen05 contraction, valid columns copied back."""
+                     c_strides, schedule, mode="auto") -> int:
+    """K and N rounded up to 16-byte multiples with zero padding (zero
+    products leave every sum unchanged), operands copied by bgx_permute into
+    aligned dense buffers, one tcgen05 contraction, valid columns copied back."""
     dev = out.device
-    kp, np_ = (K + 7) // 8 * 8, (N + 7) // 8 * 8
+    q = 16 // a.element_size()
+    kp, np_ = (K + q - 1) // q * q, (N + q - 1) // q * q
     av = torch.as_strided(a, (batch, M, K), a_strides, a.storage_offset())
     bv = torch.as_strided(b, (batch, K, N), b_strides, b.storage_offset())
     ap = torch.zeros((batch, M, kp), dtype=a.dtype, device=dev)
@@ -234,9 +241,13 @@ def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N,
         permute(cv, cp[:, :, :N], (0, 1, 2))
         cs = (M * np_, np_, 1)
     op = torch.empty((batch, M, np_), dtype=out.dtype, device=dev)
-    kind = contract_raw(ap, (M * kp, kp, 1), bp, (kp * np_, np_, 1), op, (M * np_, np_, 1),
-                        batch=batch, M=M, N=np_, K=kp, c0=cp, c_strides=cs, mode="auto",
-                        schedule=schedule)
+    contract_raw._in_pad = True
+    try:
+        kind = contract_raw(ap, (M * kp, kp, 1), bp, (kp * np_, np_, 1), op, (M * np_, np_, 1),
+                            batch=batch, M=M, N=np_, K=kp, c0=cp, c_strides=cs,
+                            mode="tc" if mode == "auto" else mode, schedule=schedule)
+    finally:
+        contract_raw._in_pad = False
     ov = torch.as_strided(out, (batch, M, N), o_strides, out.storage_offset())
     permute(op[:, :, :N], ov, (0, 1, 2))
     return kind

@@ -429,3 +429,17 @@ def test_unaligned_16bit_gemm_padded_onto_tensor_cores(dev, M, N, K, with_c0):
     big = torch.zeros(M, N + 5, device=dev, dtype=torch.bfloat16)
     contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, out=big[:, 2:N + 2])
     assert torch.equal(big[:, 2:N + 2], y)
+
+
+def test_tc_and_tf32_modes_pad_odd_shapes(dev):
+    """The tensor-core-only modes pad odd shapes instead of failing."""
+    a = torch.randn(300, 203, device=dev)
+    b = torch.randn(203, 101, device=dev)
+    y = contract("(i,k),(k,j)->(i,j)", a, b, mode="tf32")
+    want = a.double() @ b.double()
+    assert float((y.double() - want).norm() / want.norm()) <= 5e-3
+    ah, bh = a.bfloat16(), b.bfloat16()
+    executor.reset_launch_log()
+    y = contract("(i,k),(k,j)->(i,j)", ah, bh, mode="tc")
+    assert any(k.startswith("tcgen05") for k in executor.launch_log())
+    assert float((y.double() - ah.double() @ bh.double()).norm() / want.norm()) <= 1e-2
