@@ -176,7 +176,7 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
             else:
                 setattr(d.sched, k, int(v))
     kind = lib.bgx_contract_kernel(d)
-    pad_ok = a is not None and b is not None and not getattr(contract_raw, "_in_pad", False)
+    pad_ok = a is not None and b is not None and not getattr(_trace, "in_pad", False)
     if pad_ok and ((kind == _lib.KERNEL_SIMT16 and mode == "auto"
                     and 2 * batch * M * N * K >= PAD_MIN_FLOP)
                    or (kind == _lib.ERR_UNSUPPORTED and mode in ("tc", "tf32")
@@ -241,13 +241,13 @@ def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N,
         permute(cv, cp[:, :, :N], (0, 1, 2))
         cs = (M * np_, np_, 1)
     op = torch.empty((batch, M, np_), dtype=out.dtype, device=dev)
-    contract_raw._in_pad = True
+    _trace.in_pad = True     # thread-local: the padded call must not pad again
     try:
         kind = contract_raw(ap, (M * kp, kp, 1), bp, (kp * np_, np_, 1), op, (M * np_, np_, 1),
                             batch=batch, M=M, N=np_, K=kp, c0=cp, c_strides=cs,
                             mode="tc" if mode == "auto" else mode, schedule=schedule)
     finally:
-        contract_raw._in_pad = False
+        _trace.in_pad = False
     ov = torch.as_strided(out, (batch, M, N), o_strides, out.storage_offset())
     permute(op[:, :, :N], ov, (0, 1, 2))
     return kind
