@@ -139,8 +139,12 @@ typedef struct {
   int32_t max_ctas;   /* 0 = auto (persistent: one CTA per SM)              */
   int32_t raster;     /* 0 = auto; >0: groups of this many M-tiles (A slab
                          L2-resident), <0: groups of |raster| N-tiles         */
-  int32_t reserved[3]; /* reserved[0] bit 0: skip epilogue stores (timing
-                          probe only — the output is NOT written)            */
+  int32_t reserved[3]; /* reserved[0]: timing-probe bits (1 skip epilogue
+                          stores — the output is NOT written; 2 direct stores;
+                          4 skip the epilogue; 8 no start stagger).
+                          reserved[1] = cluster_n: 0 automatic, 1 one
+                          CTA pair per cluster, 2 two pairs sharing A by TMA
+                          multicast (4-CTA clusters).                         */
 } bgx_schedule;
 
 typedef struct {
