@@ -87,3 +87,16 @@ def test_ksplit_and_mshard_gloo(world):
     results = sorted(q.get() for _ in range(world))
     for rank, *oks in results:
         assert all(oks), (rank, oks)
+
+
+@pytest.mark.parametrize("M,world", [(1, 1), (300, 4), (1024, 8), (129, 8), (4096, 3), (100000, 7)])
+def test_fused_rs_row_ownership_partitions_rows(M, world):
+    """The fused reduce-scatter's ownership (rows_per_owner = ceil(M/world)
+    rounded up to 128, as bgx_contract_rs_plan computes it) covers every
+    output row exactly once, in rank order."""
+    from paper_2503_04771_b200 import shard
+    rpo = -(-(-(-M // world)) // 128) * 128
+    spans = [shard.owned_rows(M, rpo, r) for r in range(world)]
+    covered = [i for lo, hi in spans for i in range(lo, hi)]
+    assert covered == list(range(M))
+    assert all(lo <= hi for lo, hi in spans)
