@@ -161,7 +161,7 @@ def run_function(module: Module, symbol: str, inputs, step_limit=DEFAULT_STEP_LI
         tick(points * len(op.body))
         tensors = [device_of(v) for v in op.operands]
         out_t = torch.empty(tuple(vals[-1].dims), dtype=_TORCH[op.elem], device=device)
-        with torch.cuda.device(device):
+        with executor._on_device(device):
             sched = as_schedule_dict(op.schedule if op.schedule is not None else schedule)
             executor.execute(op.spec, tensors[:-1], tensors[-1], out_t, mode=mode,
                              schedule=sched)
