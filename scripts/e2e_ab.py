@@ -1,0 +1,36 @@
+"""A/B of contract_host chunking variants (used for the geometric-tail experiment,
+reverted: 17.28 vs 17.25 ms flat; the env switch no longer exists)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2503_04771_b200.api import contract_host  # noqa: E402
+
+dev = torch.device("cuda", 0)
+I, K = 32768, 8192
+hA = torch.randn(I, K).bfloat16().pin_memory()
+hB = torch.randn(K, K).bfloat16().pin_memory()
+hC = torch.randn(K, K).bfloat16().pin_memory()
+hO = torch.empty(I, K, dtype=torch.bfloat16).pin_memory()
+f = lambda: contract_host("(i,k),(k,j),(j,l)->(i,l)", hA, hB, hC, out=hO, device=dev)  # noqa: E731
+for _ in range(3):
+    f()
+res = {"tail": [], "flat": []}
+for rnd in range(6):
+    for mode in ("tail", "flat") if rnd % 2 == 0 else ("flat", "tail"):
+        if mode == "flat":
+            os.environ["BGX_E2E_NO_TAIL"] = "1"
+        else:
+            os.environ.pop("BGX_E2E_NO_TAIL", None)
+        f()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        res[mode].append((time.perf_counter() - t0) / 3 * 1e3)
+for k, v in res.items():
+    print(k, " ".join(f"{x:.2f}" for x in v), "ms  median", sorted(v)[len(v) // 2])
