@@ -5,9 +5,11 @@ Workload (``config.workload``): the sharded 32k-class chain, BASELINE config 5:
     (i,k),(k,j),(j,l)->(i,l)   I = 32768, K = J = L = 8192, bf16 in, f32
     accumulate, bf16 out; executed left to right, (A @ B) @ C
     = 2*I*J*(K+L) = 8,796,093,022,208 flop per step.
-With N GPUs (torchrun) the I rows are split into N contiguous slabs; B and C
-are replicated; there is no data-path collective; value = total flop / max
-over ranks of the device time ("scaling": "strong" — the job is fixed).
+With N GPUs (torchrun) the path partitions along I with no data-path
+collective (B and C replicated), so by default every rank runs its own
+I = 32768-row slab ("scaling": "weak": per-GPU work fixed, job = N slabs);
+``--scaling strong`` instead splits one 32768-row job into N slabs.  value =
+total flop / max over ranks of the device time.
 
 One step = one pass of the hot path over the job with inputs resident in HBM
 (the inputs, A 512 MiB and A@B 512 MiB, exceed the 126 MB L2).  ``e2e`` is the
@@ -431,6 +433,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-n", type=int, default=0)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -455,8 +458,12 @@ def main():
     _lib.load()
     pk = peaks()
 
-    r0, r1 = shard.row_range(I_, world, rank)
-    rows = r1 - r0
+    if args.scaling == "weak":
+        rows, total_rows = I_, I_ * world           # every rank: its own 32768-row slab
+    else:
+        r0, r1 = shard.row_range(I_, world, rank)
+        rows, total_rows = r1 - r0, I_
+    job_flop = 2 * total_rows * J_ * (K_ + L_)
     A, B, C = make_inputs(rows, dev, rank)
     T = torch.empty((rows, J_), dtype=torch.bfloat16, device=dev)
     O = torch.empty((rows, L_), dtype=torch.bfloat16, device=dev)
@@ -501,7 +508,7 @@ def main():
     barrier_sync(world)
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = max_over_ranks(ms_local, world)
-    value = CHAIN_FLOP / (ms * 1e-3) / 1e12
+    value = job_flop / (ms * 1e-3) / 1e12
     gemm_ms = statistics.mean(a.elapsed_time(b) for a, b in gemm_events)
     gemm_flop = 2 * rows * K_ * J_           # both launches are rows x 8192 x 8192
     achieved = gemm_flop / (gemm_ms * 1e-3) / 1e12
@@ -552,10 +559,10 @@ def main():
         c1e.record(stream)
         torch.cuda.synchronize()
         h2d_gbps = probe.numel() * 2 / (c0e.elapsed_time(c1e) * 1e-3) / 1e9
-        e2e = {"value": CHAIN_FLOP / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        e2e = {"value": job_flop / (e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e_ms,
                "h2d_bytes_per_step": (hA.numel() + hB.numel() + hC.numel()) * 2 * world,
-               "d2h_bytes_per_step": I_ * L_ * 2,
+               "d2h_bytes_per_step": total_rows * L_ * 2,
                "api": "paper_2503_04771_b200.api.contract_host (pinned host buffers)",
                "pinned_h2d_GBps_probe": h2d_gbps}
 
@@ -622,11 +629,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (torch.randn on device, bf16-rounded)",
-            "config": {"workload": WORKLOAD, "I": I_, "K": K_, "J": J_, "L": L_,
-                       "parallelism": f"M-shard x{world}",
-                       "order": "left-to-right (A@B)@C", "flop_per_step": CHAIN_FLOP,
+            "config": {"workload": WORKLOAD, "I": total_rows, "I_per_rank": rows, "K": K_,
+                       "J": J_, "L": L_, "parallelism": f"M-shard x{world}",
+                       "order": "left-to-right (A@B)@C", "flop_per_step": job_flop,
                        "flop_min_order": CHAIN_FLOP_MINORDER,
                        "l2": "inputs exceed L2 (A 512 MiB, A@B 512 MiB per 1-GPU step)"},
             "fraction_of_peak": value / (pk["bf16"] * world),
