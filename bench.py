@@ -243,7 +243,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": total_s * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "I": I_, "K": K_, "J": J_, "L": L_,
                    "parallelism": "host cores (OpenMP over outputs)",
