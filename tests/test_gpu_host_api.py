@@ -79,3 +79,37 @@ def test_contract_host_fuzz(dev):
         want = contract("(i,k),(k,j)->(i,j)", a.to(dev), b.to(dev),
                         c0=c0.to(dev) if c0 is not None else None)
         assert torch.equal(got, want.cpu()), (it, rows, K, N, pinned)
+
+
+def test_concurrent_threads_and_streams(dev):
+    """Several host threads, each on its own CUDA stream, issuing contractions
+    concurrently (per-thread launch caches and logs, thread-safe plan cache):
+    every result equals the single-threaded one."""
+    import threading
+    specs = [("(i,k),(k,j)->(i,j)", [(512, 256), (256, 384)], torch.bfloat16),
+             ("(i,j)->(j,i)", [(300, 700)], torch.float32),
+             ("(i,j)->(i)", [(200, 4000)], torch.float32),
+             ("(b,i,k),(b,k,j)->(b,i,j)", [(3, 128, 64), (3, 64, 96)], torch.float32)]
+    inputs = [[torch.randn(s, device=dev).to(dt) for s in shapes] for _, shapes, dt in specs]
+    want = [contract(sp, *xs) for (sp, _, _), xs in zip(specs, inputs)]
+    errors = []
+
+    def worker(tid):
+        try:
+            st = torch.cuda.Stream(dev)
+            with torch.cuda.stream(st):
+                for it in range(20):
+                    k = (tid + it) % len(specs)
+                    got = contract(specs[k][0], *inputs[k])
+                    st.synchronize()
+                    if not torch.equal(got, want[k]):
+                        errors.append((tid, it, specs[k][0]))
+        except Exception as e:  # noqa: BLE001
+            errors.append((tid, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:3]
