@@ -5,7 +5,9 @@ for the plumbing.
   with a free M or batch index split their output rows into contiguous slabs,
   one per rank; the other operands are replicated.  No collective on the data
   path — each rank's output slab is final.  Used for the 3-operand chain
-  (``(A_r @ B) @ C`` per rank) and the batched / plain GEMMs.
+  (``(A_r @ B) @ C`` per rank), the batched / plain GEMMs and permutations
+  (output rows of a transpose = a strided input slab); ``shard_operands`` /
+  ``lead_slabs`` cut the views.
 * K-split (``ksplit_contract``): for large-K / small-MN contractions each rank
   takes a K slab, produces f32 partial sums with the tcgen05 kernel, and the
   partials are reduced with one NCCL collective over NVLink
@@ -312,23 +314,55 @@ def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> 
 # ---------------------------------------------------------------------------
 # one process, several devices (``einsum(..., devices=...)``)
 
+def lead_slabs(spec, operands, lo: int, hi: int):
+    """Views of ``operands`` restricted to rows ``[lo, hi)`` of the output's
+    leading index (§8e): every operand that carries that index is narrowed
+    along it (a strided view when it is not the operand's first axis — e.g.
+    the input columns of a transpose ``(i,j)->(j,i)``), the rest are returned
+    whole.  The output's leading index is parallel (it is an output index), so
+    output rows ``[lo, hi)`` depend on nothing else and every element is
+    evaluated exactly as in the unsharded call."""
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    if not spec.output:
+        raise ValueError(f"{spec}: a rank-0 output has no rows to shard")
+    lead = spec.output[0]
+    return [t.narrow(tup.index(lead), lo, hi - lo) if lead in tup else t
+            for t, tup in zip(operands, spec.inputs)]
+
+
+def shard_operands(spec, operands, world: int, rank: int, align: int = 128):
+    """One-process-per-GPU form of the M-shard: rank ``rank``'s output row
+    range ``(lo, hi)`` (``row_range`` of the output's leading extent) and the
+    operand views that produce it (``lead_slabs``)."""
+    from .api import output_shape
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    rows = output_shape(spec, operands)[0] if spec.output else 0
+    lo, hi = row_range(rows, world, rank, align)
+    return lo, hi, lead_slabs(spec, operands, lo, hi)
+
+
 def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> torch.Tensor:
     """M-sharded contraction driven from ONE process over ``devices``: rows of
-    the output's leading index (which must come only from operand 0) are split
-    into contiguous slabs (``row_range``); slab r of operand 0 and a replica
-    of every other operand go to ``devices[r]`` (peer copies over NVLink), each
-    device contracts its slab on its own current stream — launches are
-    asynchronous, so the devices run concurrently — and the slabs are copied
-    back into ``out`` on the operands' device.  No collective: the slabs are
-    independent (the §8e M-shard), so every row is computed as on one device —
-    bit for bit unless the planner splits K differently for a slab (long K),
-    which only reorders the f32 summation."""
-    from .api import _row_streamable, output_shape
+    the output's leading index are split into contiguous slabs
+    (``row_range``); the operand views that produce slab r (``lead_slabs``:
+    narrowed along that index, the other operands whole) are copied to
+    ``devices[r]`` (peer copies over NVLink), each device contracts its slab
+    on its own current stream — launches are asynchronous, so the devices run
+    concurrently — and the slabs are copied back into ``out`` on the
+    operands' device.  Covers contractions (leading index from operand 0, 1,
+    or several operands) and permutations (a transpose's output rows are a
+    strided column slab of its input, §8e).  No collective: the slabs are
+    independent, so every row is computed as on one device — bit for bit
+    unless the planner splits K differently for a slab (long K), which only
+    reorders the f32 summation."""
+    from .api import output_shape
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
     devices = [torch.device("cuda", d) if isinstance(d, int) else torch.device(d) for d in devices]
-    if not _row_streamable(spec, operands):
-        raise ValueError(f"{spec}: the output's leading index must come from operand 0 only")
+    if not spec.output:
+        raise ValueError(f"{spec}: a rank-0 output has no rows to shard")
     home = operands[0].device
     shape = output_shape(spec, operands)
     dt = kw.get("out_dtype") or operands[0].dtype
@@ -343,10 +377,9 @@ def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> 
         if hi <= lo:
             continue
         with torch.cuda.device(dev):
-            a = operands[0][lo:hi].to(dev, non_blocking=True)
-            others = [t.to(dev, non_blocking=True) for t in operands[1:]]
+            local = [t.to(dev, non_blocking=True) for t in lead_slabs(spec, operands, lo, hi)]
             cc = c0[lo:hi].to(dev, non_blocking=True) if c0 is not None else None
-            y = contract(spec, a, *others, c0=cc, **kw)
+            y = contract(spec, *local, c0=cc, **kw)
             done = torch.cuda.Event()
             done.record(torch.cuda.current_stream(dev))
         pending.append((lo, hi, y, done))

@@ -55,8 +55,34 @@ def test_contract_devices_matches_single_device(dev):
     for devs in ([0, 0], [0, 0, 0]):
         sh = contract(spec, a, b, c, devices=devs, schedule={"splits": 1})
         assert torch.equal(sh, whole)
-    with pytest.raises(ValueError, match="leading index"):
-        contract("(k,i),(k,j)->(i,j)", a.t(), b, devices=[0, 0])
+    # leading output index not the first axis of operand 0 (strided slab)
+    at = a.t().contiguous()
+    whole = contract("(k,i),(k,j)->(i,j)", at, b, schedule={"splits": 1})
+    assert torch.equal(contract("(k,i),(k,j)->(i,j)", at, b, devices=[0, 0],
+                                schedule={"splits": 1}), whole)
+    # leading output index carried by operand 1
+    whole = contract("(k,j),(i,k)->(i,j)", b, a, schedule={"splits": 1})
+    assert torch.equal(contract("(k,j),(i,k)->(i,j)", b, a, devices=[0, 0, 0],
+                                schedule={"splits": 1}), whole)
+    with pytest.raises(ValueError, match="rank-0"):
+        contract("(i),(i)->()", a[:, 0], a[:, 1], devices=[0, 0])
+
+
+@pytest.mark.parametrize("spec,shape", [("(i,j)->(j,i)", (1000, 777)),
+                                        ("(i,j,k)->(k,j,i)", (33, 64, 130)),
+                                        ("(i,j,k)->(j,k,i)", (17, 300, 9))])
+def test_contract_devices_permutation(dev, spec, shape):
+    """§8e permutation shard: each device writes a slab of output rows from a
+    strided slab of the input — bit-exact against the unsharded kernel and
+    torch's own permute."""
+    from paper_2503_04771_b200.einsum import parse_einsum
+    x = torch.randn(shape, device=dev)
+    sp = parse_einsum(spec)
+    perm = [sp.inputs[0].index(ax) for ax in sp.output]
+    want = x.permute(perm).contiguous()
+    assert torch.equal(contract(spec, x), want)
+    for devs in ([0, 0], [0, 0, 0, 0]):
+        assert torch.equal(contract(spec, x, devices=devs), want)
 
 
 def test_contract_host_fuzz(dev):

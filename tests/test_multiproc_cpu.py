@@ -100,3 +100,67 @@ def test_fused_rs_row_ownership_partitions_rows(M, world):
     covered = [i for lo, hi in spans for i in range(lo, hi)]
     assert covered == list(range(M))
     assert all(lo <= hi for lo, hi in spans)
+
+
+_SHARD_SPECS = [("(i,k),(k,j)->(i,j)", [(300, 40), (40, 24)]),
+                ("(k,i),(k,j)->(i,j)", [(40, 300), (40, 24)]),
+                ("(k,j),(i,k)->(i,j)", [(40, 24), (300, 40)]),
+                ("(i,j)->(j,i)", [(50, 333)]),
+                ("(i,j,k)->(k,j,i)", [(7, 9, 260)]),
+                ("(i,k),(k,j),(j,l)->(i,l)", [(257, 16), (16, 8), (8, 12)])]
+
+
+def _torch_einsum(spec, ops):
+    """CPU stand-in for the per-rank contraction (bracket spec -> torch.einsum)."""
+    from paper_2503_04771_b200.einsum import parse_einsum
+    sp = parse_einsum(spec)
+    letters = {ax: chr(97 + n) for n, ax in enumerate(sp.axes)}
+    eq = ",".join("".join(letters[a] for a in t) for t in sp.inputs)
+    return torch.einsum(eq + "->" + "".join(letters[a] for a in sp.output), *ops)
+
+
+def _shard_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oks = []
+        for n, (spec, shapes) in enumerate(_SHARD_SPECS):
+            g = torch.Generator().manual_seed(n)
+            ops = [torch.randn(s, generator=g, dtype=torch.float64) for s in shapes]
+            lo, hi, local = shard.shard_operands(spec, ops, world, rank, align=16)
+            mine = _torch_einsum(spec, local)
+            parts = [None] * world
+            dist.all_gather_object(parts, (lo, hi, mine))
+            stitched = torch.cat([p[2] for p in sorted(parts, key=lambda t: t[0])])
+            oks.append(torch.allclose(stitched, _torch_einsum(spec, ops), rtol=1e-12, atol=1e-12))
+        q.put((rank, *oks))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_shard_operands_gloo(world):
+    """§8e M-shard for any leading output index (operand 0 or 1, strided
+    slabs, permutations, the chain): stitched per-rank slabs equal the whole."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for rank, *oks in sorted(q.get() for _ in range(world)):
+        assert all(oks), (rank, oks)
+
+
+def test_lead_slabs_views():
+    """lead_slabs narrows exactly the operands carrying the output's leading
+    index, along that index, without copying."""
+    a, b = torch.randn(40, 300), torch.randn(40, 24)
+    sa, sb = shard.lead_slabs("(k,i),(k,j)->(i,j)", [a, b], 100, 164)
+    assert sa.shape == (40, 64) and sa.data_ptr() == a[:, 100:].data_ptr() and sb is b
+    with pytest.raises(ValueError, match="rank-0"):
+        shard.lead_slabs("(i),(i)->()", [a[0], a[1]], 0, 1)
