@@ -34,6 +34,13 @@
 #include <mutex>
 #include <string.h>
 
+// 512-wide pair tiles: read both TMEM halves into packed registers before any
+// store (0 = read, release and store one half at a time).  A/B on B200:
+// 4096^3 forced to 512 tiles +1.8 % burst, other shapes neutral.
+#ifndef BGX_EPI_DRAIN_BOTH
+#define BGX_EPI_DRAIN_BOTH 1
+#endif
+
 namespace bgx {
 
 namespace {
@@ -671,6 +678,28 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           // warp, and only then stage + TMA-store — the stores (and their
           // buffer waits) leave the MMA critical path.
           constexpr int PER_HALF = NCHUNK / 2 / 2;  // chunks per warp per half
+#if BGX_EPI_DRAIN_BOTH
+          // drain BOTH halves into registers before any store: the next
+          // tile's second-half MMAs wait only for the TMEM reads
+          uint32_t pk2[2][PER_HALF][16];
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+#pragma unroll
+            for (int j = 0; j < PER_HALF; ++j) {
+              const int c = half * (NCHUNK / 2) + g + 2 * j;
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(taddr + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int q = 0; q < 16; ++q)
+                pk2[half][j][q] = pack2<OutT>(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+            }
+            arrive_empty(half);
+          }
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t (&pk)[PER_HALF][16] = pk2[half];
+#else
 #pragma unroll 1
           for (int half = 0; half < 2; ++half) {
             uint32_t pk[PER_HALF][16];
@@ -685,6 +714,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                 pk[j][q] = pack2<OutT>(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
             }
             arrive_empty(half);   // this half of TMEM is free for the next tile
+#endif
 #pragma unroll
             for (int j = 0; j < PER_HALF; ++j) {
               const int c = half * (NCHUNK / 2) + g + 2 * j;

@@ -3,6 +3,7 @@ RTLD_LOCAL) plus cuBLAS, interleaved, on the BASELINE GEMM shapes: burst
 (after 1 s idle, median of 20) and sustained (~2 s back to back, median of
 the second half) with the NVML SM clock.  Usage:
     python scripts/ab_lib.py NEW.so OLD.so [shape,shape...]
+(AB_SCHED="tile_n=512,cta_group=2" forces a schedule on both builds.)
 """
 import ctypes
 import json
@@ -42,6 +43,14 @@ def launcher(lib, a, b, out, bt, M, N, K):
     d.o_stride[:] = [M * N, N, 1]
     d.in_dtype = d.out_dtype = _lib.BF16
     d.mode = _lib.MODE_TC
+    sched = os.environ.get("AB_SCHED")   # e.g. "tile_n=512,cta_group=2"
+    if sched:
+        from paper_2503_04771_b200.schedule import Schedule
+        for k, v in Schedule.parse(sched).to_dict().items():
+            if k == "cluster_n":
+                d.sched.reserved[1] = v
+            elif k != "splits":
+                setattr(d.sched, k, v)
     st = torch.cuda.current_stream().cuda_stream
 
     def run():
