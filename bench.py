@@ -381,7 +381,21 @@ def ksplit_aux(dev, world, rank):
     g = torch.Generator(device=dev).manual_seed(11 + rank)
     a = torch.randn(M, Kr, device=dev, generator=g).bfloat16()
     b = torch.randn(Kr, N, device=dev, generator=g).bfloat16()
-    fused = shard.FusedKSplit(spec, a, b)
+    # every rank must have built its fused plan before any rank enters the
+    # symmetric-memory barriers inside the calls (a rank that failed here and
+    # skipped them would leave the others spinning on the device)
+    err = None
+    try:
+        fused = shard.FusedKSplit(spec, a, b)
+    except Exception as e:  # noqa: BLE001
+        err = f"{type(e).__name__}: {e}"[:300]
+    if world > 1:
+        flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            return {"skipped": err or "FusedKSplit construction failed on another rank"}
+    elif err:
+        return {"error": err}
     res = {"shape": {"M": M, "N": N, "K_per_rank": Kr, "world": world},
            "plan": {"cta_group": fused.plan.cta_group, "tile_n": fused.plan.tile_n,
                     "rows_per_owner": fused.plan.rows_per_owner,
