@@ -210,15 +210,35 @@ BGX_API int bgx_contract_splitk(const bgx_contract_desc *d, int32_t splits, void
  * with local buffers (rank 0..world-1 in stream order) compute exactly what
  * `world` GPUs would.  bgx_contract_rs_plan fills tile shape, rows_per_owner,
  * local_splits and the buffer sizes for a (M, N, K_r, world) problem; every
- * rank must use the same plan.                                              */
+ * rank must use the same plan.
+ *
+ * plan.mode selects where the sums happen:
+ *   BGX_RS_IN_KERNEL (0): as above — the last arriver reduces inside the
+ *     kernel (levels 1 and 2);
+ *   BGX_RS_DEFERRED (1, the planner's choice): the kernel only delivers —
+ *     every (rank, local slice) unit stores its f32 partial tile straight
+ *     into  slots[owner] + ((rank * local_splits + slice) * rows_per_owner
+ *     + local_row) * N  (no counters, no ws); after the caller's barrier
+ *     each owner runs bgx_rs_reduce, one all-SM kernel that sums its slots
+ *     slice-major inside each rank, ranks in rank order (the same order as
+ *     mode 0, so both modes are bit-identical), adds c0, casts and stores
+ *     its out rows.  The serial tail of the last arrivers (latency-bound
+ *     remote reads by a few CTAs) becomes one bandwidth-bound local pass.
+ *     slot_bytes = world * local_splits * rows_per_owner * N * 4, ws_bytes 0.
+ * bgx_rs_reduce(d, rs, stream) reduces owner rs->plan.rank (mode 1 only).  */
+#define BGX_RS_IN_KERNEL 0
+#define BGX_RS_DEFERRED 1
 #define BGX_MAX_RANKS 8
 typedef struct {
   int32_t world, rank;
   int32_t cta_group, tile_n;     /* tile shape (from the plan)               */
   int32_t local_splits;          /* >= 1                                     */
   int32_t out_dtype;             /* bgx_dtype of out / c0                    */
+  int32_t mode;                  /* BGX_RS_IN_KERNEL / BGX_RS_DEFERRED       */
+  int32_t reserved0;
   int64_t rows_per_owner;
-  int64_t slot_bytes;            /* per owner: world * rows_per_owner * N * 4 */
+  int64_t slot_bytes;            /* per owner: world * rows_per_owner * N * 4
+                                    (mode 1: x local_splits)                 */
   int64_t counter_bytes;         /* per owner and for ws_counters            */
   int64_t ws_bytes;              /* local: local_splits * M * N * 4 (or 0)   */
 } bgx_rs_plan;
@@ -234,6 +254,7 @@ typedef struct {
 BGX_API int bgx_contract_rs_plan(const bgx_contract_desc *d, int32_t world, bgx_rs_plan *plan);
 BGX_API int bgx_contract_reduce_scatter(const bgx_contract_desc *d, const bgx_reduce_scatter *rs,
                                         void *stream);
+BGX_API int bgx_rs_reduce(const bgx_contract_desc *d, const bgx_reduce_scatter *rs, void *stream);
 
 /* ---- elementwise helpers for multi-GPU K-split -------------------------
  * out[i] = (dtype_out) src[i] for n elements, src f32 (the reduced partials),

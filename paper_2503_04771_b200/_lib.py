@@ -63,9 +63,13 @@ class BgxContractDesc(ctypes.Structure):
                 ("sched", BgxSchedule)]
 
 
+RS_IN_KERNEL, RS_DEFERRED = 0, 1     # bgx_rs_plan.mode
+
+
 class BgxRsPlan(ctypes.Structure):
     _fields_ = [("world", _i32), ("rank", _i32), ("cta_group", _i32), ("tile_n", _i32),
-                ("local_splits", _i32), ("out_dtype", _i32), ("rows_per_owner", _i64),
+                ("local_splits", _i32), ("out_dtype", _i32), ("mode", _i32), ("reserved0", _i32),
+                ("rows_per_owner", _i64),
                 ("slot_bytes", _i64), ("counter_bytes", _i64), ("ws_bytes", _i64)]
 
 
@@ -95,6 +99,8 @@ SIGNATURES = {
                                             ctypes.POINTER(BgxRsPlan)]),
     "bgx_contract_reduce_scatter": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
                                                    ctypes.POINTER(BgxReduceScatter), _vp]),
+    "bgx_rs_reduce": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc),
+                                     ctypes.POINTER(BgxReduceScatter), _vp]),
     "bgx_cast_f32": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _vp]),
     "bgx_clock_sample": (ctypes.c_int, [_vp, _vp]),
     "bgx_rtc_compile": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p,

@@ -11,6 +11,7 @@ int contract_tc_splitk(const bgx_contract_desc &d, int splits, void *ws, int64_t
                        cudaStream_t s);
 int tc_rs_plan(const bgx_contract_desc &d, int world, bgx_rs_plan *pl);
 int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cudaStream_t s);
+int rs_reduce(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cudaStream_t s);
 
 namespace {
 
@@ -166,4 +167,10 @@ extern "C" int bgx_contract_reduce_scatter(const bgx_contract_desc *d, const bgx
   BGX_CHECK_ARG(d->M > 0 && d->N > 0 && d->K > 0, "bgx_contract_reduce_scatter: empty extent");
   BGX_CHECK_ARG(d->a != nullptr && d->b != nullptr, "bgx_contract_reduce_scatter: null operand");
   return contract_tc_rs(*d, *rs, (cudaStream_t)stream);
+}
+
+extern "C" int bgx_rs_reduce(const bgx_contract_desc *d, const bgx_reduce_scatter *rs, void *stream) {
+  BGX_CHECK_ARG(d && rs, "bgx_rs_reduce: null argument");
+  BGX_CHECK_ARG(d->M > 0 && d->N > 0 && d->K > 0, "bgx_rs_reduce: empty extent");
+  return rs_reduce(*d, *rs, (cudaStream_t)stream);
 }

@@ -86,6 +86,7 @@ struct TcParams {
   void *out; int64_t so[3];
   // fused K-split reduce-scatter epilogue (RS kernels only, bgx.h)
   int32_t rs_world, rs_rank, rs_out_dtype;
+  int32_t rs_defer;                     // BGX_RS_DEFERRED: deliver only (bgx_rs_reduce sums)
   int64_t rs_rpo;                       // output rows per owner
   float *rs_slots[BGX_MAX_RANKS];
   uint32_t *rs_counters[BGX_MAX_RANKS];
@@ -191,6 +192,13 @@ __device__ __forceinline__ UnitInfo unit_info(const TcParams &p, int64_t u) {
   }
   r.t = u % p.num_tiles;
   r.kslice = u / p.num_tiles;
+  if (p.kb_per_split == 0) {
+    // balanced partition (fused reduce-scatter): exactly k_splits non-empty
+    // slices (k_splits <= k_blocks)
+    r.kb_lo = (int)(r.kslice * p.k_blocks / p.k_splits);
+    r.nkb = (int)((r.kslice + 1) * p.k_blocks / p.k_splits) - r.kb_lo;
+    return r;
+  }
   r.kb_lo = (int)r.kslice * p.kb_per_split;
   const int hi = r.kb_lo + p.kb_per_split < p.k_blocks ? r.kb_lo + p.kb_per_split : p.k_blocks;
   r.nkb = hi - r.kb_lo;
@@ -579,7 +587,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         const int64_t cidx = t * CG + rank;   // one counter per CTA half of a tile
         const int S = p.k_splits;
         float *slot_row = p.rs_slots[owner] + ((int64_t)p.rs_rank * p.rs_rpo + lrow) * p.N;
-        float *dst = S > 1 ? p.ws + (ui.kslice * p.M + m) * p.N : slot_row;
+        float *dst = p.rs_defer
+            ? p.rs_slots[owner] + (((int64_t)p.rs_rank * S + ui.kslice) * p.rs_rpo + lrow) * p.N
+            : (S > 1 ? p.ws + (ui.kslice * p.M + m) * p.N : slot_row);
         // (1) TMEM -> f32 partial rows (local split slice, or straight into
         //     the owner's slot over NVLink)
         uint32_t rbuf[2][32];
@@ -598,6 +608,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         }
         tmem_ld_wait();
         arrive_empty(acc);
+        if (p.rs_defer) continue;   // delivered; the owner's bgx_rs_reduce sums
         // a CTA half entirely below the last output row has no owner (its
         // rows do not exist): nothing to deliver, no counter to bump
         if (tm * C::TILE_M + rank * BM >= p.M) continue;
@@ -959,8 +970,15 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   p.tiles_n = (int32_t)(((d.N + BN - 1) / BN + CN - 1) / CN);   // schedule units along N
   p.num_tiles = (int64_t)p.tiles_m * p.tiles_n * d.batch;
   if (p.k_splits < 1) p.k_splits = 1;
-  p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
-  p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
+  if (RS) {
+    // fused reduce-scatter: balanced slices, count kept (unit_info), so both
+    // reduction placements sum the same slices and every rank fills the
+    // same number of deferred slots
+    p.kb_per_split = 0;
+  } else {
+    p.kb_per_split = (p.k_blocks + p.k_splits - 1) / p.k_splits;
+    p.k_splits = (p.k_blocks + p.kb_per_split - 1) / p.kb_per_split;
+  }
   p.num_units = p.num_tiles * p.k_splits;
   auto kern = tc_gemm_kernel<BN, CG, OutT, IN_BYTES, RS, CN>;
   constexpr int CL = CG * CN;
@@ -1329,10 +1347,147 @@ int tc_rs_plan(const bgx_contract_desc &d, int world, bgx_rs_plan *pl) {
   if (sp < 1) sp = 1;
   pl->local_splits = (int32_t)sp;
   pl->out_dtype = d.out_dtype;
-  pl->slot_bytes = (int64_t)world * pl->rows_per_owner * d.N * 4;
+  pl->mode = BGX_RS_DEFERRED;
+  pl->slot_bytes = (int64_t)world * sp * pl->rows_per_owner * d.N * 4;
   pl->counter_bytes = (tiles * cg * 4 + 15) / 16 * 16;
-  pl->ws_bytes = sp > 1 ? sp * d.M * d.N * 4 : 0;
+  pl->ws_bytes = 0;
   return BGX_OK;
+}
+
+// ---- deferred reduce-scatter: the owner's all-SM reduction ------------------
+// out[r][j] = cast( (((sum_s slot[0][s]) + sum_s slot[1][s]) + ...) + c0 ),
+// every inner sum slice-ordered from slice 0 — the order of the in-kernel mode.
+template <typename OutT>
+__global__ void rs_reduce_kernel(const float *__restrict__ slots, const OutT *__restrict__ c0,
+                                 OutT *__restrict__ out, int64_t rows, int64_t N, int64_t rpo,
+                                 int world, int S, int64_t so, int64_t sc) {
+  const int64_t total = rows * N;
+  const int64_t plane = rpo * N;           // one (rank, slice) partial
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, j = i - r * N;
+    const float *src = slots + r * N + j;
+    float acc = 0.f;
+    for (int rk = 0; rk < world; ++rk) {
+      float part = __ldg(src + (int64_t)rk * S * plane);
+      for (int sl = 1; sl < S; ++sl) part = __fadd_rn(part, __ldg(src + ((int64_t)rk * S + sl) * plane));
+      acc = rk == 0 ? part : __fadd_rn(acc, part);
+    }
+    if (c0) acc = __fadd_rn(acc, Conv<OutT>::to_f(c0[r * sc + j]));
+    out[r * so + j] = Conv<OutT>::from_f(acc);
+  }
+}
+
+// Vector form (N % 4 == 0, 16-byte aligned slots): thread (x, y) sums rank y's
+// S slices of 4 columns (loads batched four slices at a time, so every
+// thread keeps 64 bytes in flight), the ranks' partials meet in shared memory
+// and lane y = 0 adds them in rank order, adds c0, casts and stores.
+constexpr int RSR_X = 64;
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                     __fadd_rn(a.w, b.w));
+}
+template <typename OutT>
+__global__ void __launch_bounds__(RSR_X * BGX_MAX_RANKS)
+rs_reduce_vec_kernel(const float *__restrict__ slots, const OutT *__restrict__ c0,
+                     OutT *__restrict__ out, int64_t rows, int64_t N, int64_t rpo, int S,
+                     int64_t so, int64_t sc) {
+  __shared__ float4 part[BGX_MAX_RANKS][RSR_X];
+  const int64_t nq = N / 4;
+  const int64_t q = blockIdx.x * (int64_t)RSR_X + threadIdx.x;
+  const int rk = threadIdx.y, world = blockDim.y;
+  const int64_t r = q / nq, j = (q - r * nq) * 4;
+  const bool ok = r < rows;
+  if (ok) {
+    const int64_t plane = rpo * N;
+    const float4 *src = reinterpret_cast<const float4 *>(slots + ((int64_t)rk * S * rpo + r) * N + j);
+    const int64_t pstep = plane / 4;   // float4s per slice plane
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    int sl = 0;
+    for (; sl + 4 <= S; sl += 4) {            // four slices' loads in flight
+      const float4 x0 = __ldg(src + sl * pstep), x1 = __ldg(src + (sl + 1) * pstep);
+      const float4 x2 = __ldg(src + (sl + 2) * pstep), x3 = __ldg(src + (sl + 3) * pstep);
+      p = f4_add(f4_add(f4_add(sl == 0 ? x0 : f4_add(p, x0), x1), x2), x3);
+    }
+    for (; sl < S; ++sl) {
+      const float4 x = __ldg(src + sl * pstep);
+      p = sl == 0 ? x : f4_add(p, x);
+    }
+    part[rk][threadIdx.x] = p;
+  }
+  __syncthreads();
+  if (!ok || rk != 0) return;
+  float4 acc = part[0][threadIdx.x];
+  for (int k = 1; k < world; ++k) acc = f4_add(acc, part[k][threadIdx.x]);
+  float v[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (c0) v[e] = __fadd_rn(v[e], Conv<OutT>::to_f(c0[r * sc + j + e]));
+    out[r * so + j + e] = Conv<OutT>::from_f(v[e]);
+  }
+}
+
+int rs_reduce(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cudaStream_t s) {
+  const bgx_rs_plan &pl = rs.plan;
+  BGX_CHECK_ARG(pl.mode == BGX_RS_DEFERRED, "bgx_rs_reduce: plan mode %d is not deferred", pl.mode);
+  BGX_CHECK_ARG(pl.world >= 1 && pl.world <= BGX_MAX_RANKS && pl.rank >= 0 && pl.rank < pl.world,
+                "bgx_rs_reduce: rank %d of %d", pl.rank, pl.world);
+  BGX_CHECK_ARG(pl.local_splits >= 1 && pl.rows_per_owner > 0, "bgx_rs_reduce: bad plan");
+  const int S = pl.local_splits;        // every rank delivered exactly S slices
+  const int r = pl.rank;
+  BGX_CHECK_ARG(rs.slots[r] && rs.out[r], "bgx_rs_reduce: null slot/out for owner %d", r);
+  int64_t rows = d.M - (int64_t)r * pl.rows_per_owner;
+  if (rows > pl.rows_per_owner) rows = pl.rows_per_owner;
+  if (rows <= 0) return BGX_OK;          // an owner past the last row has nothing
+  const int64_t total = rows * d.N;
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = (int64_t)sm_count_current() * 8;
+  if (blocks > cap) blocks = cap;
+  const int64_t so = d.o_stride[1], sc = d.c_stride[1];
+  if (d.N % 4 == 0 && ((uintptr_t)rs.slots[r] & 15) == 0) {
+    const dim3 blk(RSR_X, pl.world);
+    const unsigned grid = (unsigned)((total / 4 + RSR_X - 1) / RSR_X);
+    const int64_t rpo = pl.rows_per_owner;
+    switch (pl.out_dtype) {
+      case BGX_F32:
+        rs_reduce_vec_kernel<float><<<grid, blk, 0, s>>>(rs.slots[r], (const float *)rs.c0[r],
+                                                         (float *)rs.out[r], rows, d.N, rpo, S, so, sc);
+        return check_launch("rs_reduce_vec_kernel");
+      case BGX_BF16:
+        rs_reduce_vec_kernel<__nv_bfloat16><<<grid, blk, 0, s>>>(
+            rs.slots[r], (const __nv_bfloat16 *)rs.c0[r], (__nv_bfloat16 *)rs.out[r], rows, d.N,
+            rpo, S, so, sc);
+        return check_launch("rs_reduce_vec_kernel");
+      case BGX_F16:
+        rs_reduce_vec_kernel<__half><<<grid, blk, 0, s>>>(rs.slots[r], (const __half *)rs.c0[r],
+                                                          (__half *)rs.out[r], rows, d.N, rpo, S,
+                                                          so, sc);
+        return check_launch("rs_reduce_vec_kernel");
+      default:
+        break;
+    }
+  }
+  switch (pl.out_dtype) {
+    case BGX_F32:
+      rs_reduce_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
+          rs.slots[r], (const float *)rs.c0[r], (float *)rs.out[r], rows, d.N, pl.rows_per_owner,
+          pl.world, S, so, sc);
+      break;
+    case BGX_BF16:
+      rs_reduce_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, s>>>(
+          rs.slots[r], (const __nv_bfloat16 *)rs.c0[r], (__nv_bfloat16 *)rs.out[r], rows, d.N,
+          pl.rows_per_owner, pl.world, S, so, sc);
+      break;
+    case BGX_F16:
+      rs_reduce_kernel<__half><<<(unsigned)blocks, 256, 0, s>>>(
+          rs.slots[r], (const __half *)rs.c0[r], (__half *)rs.out[r], rows, d.N, pl.rows_per_owner,
+          pl.world, S, so, sc);
+      break;
+    default:
+      set_error("bgx_rs_reduce: out dtype %d", pl.out_dtype);
+      return BGX_ERR_INVALID;
+  }
+  return check_launch("rs_reduce_kernel");
 }
 
 int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cudaStream_t s) {
@@ -1350,7 +1505,10 @@ int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cud
   BGX_CHECK_ARG(pl.rows_per_owner > 0 && pl.rows_per_owner % BM == 0 &&
                     pl.rows_per_owner * pl.world >= d.M,
                 "reduce-scatter: rows_per_owner %lld", (long long)pl.rows_per_owner);
-  BGX_CHECK_ARG(pl.local_splits >= 1 && (pl.local_splits == 1 || (rs.ws && rs.ws_counters)),
+  BGX_CHECK_ARG(pl.mode == BGX_RS_IN_KERNEL || pl.mode == BGX_RS_DEFERRED,
+                "reduce-scatter: mode %d", pl.mode);
+  BGX_CHECK_ARG(pl.local_splits >= 1 && (pl.local_splits == 1 || pl.mode == BGX_RS_DEFERRED ||
+                                         (rs.ws && rs.ws_counters)),
                 "reduce-scatter: local split workspace missing");
   for (int r = 0; r < pl.world; ++r)
     BGX_CHECK_ARG(rs.slots[r] && rs.counters[r] && rs.out[r],
@@ -1369,6 +1527,11 @@ int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cud
   p.a_mn = d.a_stride[2] != 1 ? 1 : 0;
   p.b_mn = d.b_stride[2] == 1 ? 1 : 0;
   p.k_blocks = (int32_t)((d.K + Elem<2>::BK - 1) / Elem<2>::BK);
+  // deferred mode: the owners' reduction reads exactly local_splits slices
+  // from every rank, so every rank must be able to fill them
+  BGX_CHECK_ARG(pl.mode != BGX_RS_DEFERRED || pl.local_splits <= p.k_blocks,
+                "reduce-scatter: local_splits %d > %d k-blocks of this rank's slab (deferred "
+                "mode needs local_splits <= every rank's k-blocks)", pl.local_splits, p.k_blocks);
   p.k_splits = pl.local_splits > p.k_blocks ? p.k_blocks : pl.local_splits;
   p.tail_splits = 1;
   p.ws = rs.ws;
@@ -1377,6 +1540,7 @@ int contract_tc_rs(const bgx_contract_desc &d, const bgx_reduce_scatter &rs, cud
   p.debug = d.sched.reserved[0];
   p.rs_world = pl.world;
   p.rs_rank = pl.rank;
+  p.rs_defer = pl.mode == BGX_RS_DEFERRED ? 1 : 0;
   p.rs_out_dtype = pl.out_dtype;
   p.rs_rpo = pl.rows_per_owner;
   for (int r = 0; r < BGX_MAX_RANKS; ++r) {

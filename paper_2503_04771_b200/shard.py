@@ -170,6 +170,24 @@ def rs_plan(spec, a_slab, b_slab, world: int, out_dtype=None) -> _lib.BgxRsPlan:
     return pl
 
 
+_BK = 64   # bf16/f16 elements per tcgen05 k-block (gemm_tc.cu Elem<2>::BK)
+
+
+def _finish_plan(pl, M: int, N: int, splits: int, mode: int | None):
+    """Set the agreed local split (and mode) on a plan and recompute the
+    buffer sizes that depend on them (bgx.h bgx_rs_plan)."""
+    if mode is not None:
+        pl.mode = mode
+    pl.local_splits = max(1, int(splits))
+    S, rpo = pl.local_splits, pl.rows_per_owner
+    if pl.mode == _lib.RS_DEFERRED:
+        pl.slot_bytes, pl.ws_bytes = pl.world * S * rpo * N * 4, 0
+    else:
+        pl.slot_bytes = pl.world * rpo * N * 4
+        pl.ws_bytes = S * M * N * 4 if S > 1 else 0
+    return pl
+
+
 def owned_rows(M: int, rows_per_owner: int, rank: int):
     """Output rows [lo, hi) the fused reduce-scatter leaves on ``rank``."""
     lo = min(M, rank * rows_per_owner)
@@ -191,7 +209,8 @@ class FusedKSplit:
     ``reduce_scatter_tensor`` -> cast) with no NCCL on the data path."""
 
     def __init__(self, spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *, out_dtype=None,
-                 group=None, with_c0: bool = False):
+                 group=None, with_c0: bool = False, local_splits: int | None = None,
+                 mode: int | None = None):
         self.spec = spec if isinstance(spec, EinsumSpec) else parse_einsum(spec)
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -204,6 +223,18 @@ class FusedKSplit:
         pl = _lib.BgxRsPlan()
         _lib.check(self._lib.bgx_contract_rs_plan(d, self.world, pl), "bgx_contract_rs_plan")
         pl.rank = self.rank
+        if local_splits is not None and local_splits < 1:
+            raise ValueError(f"local_splits must be >= 1, got {local_splits}")
+        # every rank must use the same local split (deferred mode: it fixes
+        # the slot layout) and it may not exceed any rank's k-blocks
+        S = local_splits if local_splits is not None else pl.local_splits
+        kb = -(-p.K // _BK)
+        if self.world > 1:
+            dev = self.dev if dist.get_backend(group) == "nccl" else torch.device("cpu")
+            t = torch.tensor([S, kb], dtype=torch.int64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            S, kb = int(t[0]), int(t[1])
+        _finish_plan(pl, self.M, self.N, min(S, kb), mode)
         self.plan = pl
         rpo, N = pl.rows_per_owner, self.N
         esz = torch.tensor([], dtype=self.out_dtype).element_size()
@@ -232,7 +263,7 @@ class FusedKSplit:
             rs.out[r] = base + offs["out"]
             rs.c0[r] = base + offs["c0"] if with_c0 else None
         self.ws = None
-        if pl.local_splits > 1:
+        if pl.ws_bytes > 0:             # in-kernel mode with a local split
             self.ws = torch.empty(pl.ws_bytes, dtype=torch.uint8, device=self.dev)
             self.ws_counters = torch.zeros(max(16, pl.counter_bytes), dtype=torch.uint8,
                                            device=self.dev)
@@ -256,22 +287,28 @@ class FusedKSplit:
         self.desc.b = ins[1 - self._a_idx].data_ptr()
         if self.hdl is not None:
             self.hdl.barrier()
-        _lib.check(self._lib.bgx_contract_reduce_scatter(
-            self.desc, self.rs, torch.cuda.current_stream(self.dev).cuda_stream),
-            "bgx_contract_reduce_scatter")
+        stream = torch.cuda.current_stream(self.dev).cuda_stream
+        _lib.check(self._lib.bgx_contract_reduce_scatter(self.desc, self.rs, stream),
+                   "bgx_contract_reduce_scatter")
         executor._log("tcgen05-rs")
         if self.hdl is not None:
             self.hdl.barrier()
+        if self.plan.mode == _lib.RS_DEFERRED:   # every partial of my rows is in my slots
+            _lib.check(self._lib.bgx_rs_reduce(self.desc, self.rs, stream), "bgx_rs_reduce")
+            executor._log("rs-reduce")
         return self.out
 
 
-def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> torch.Tensor:
+def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None,
+                         mode: int | None = None, local_splits: int | None = None) -> torch.Tensor:
     """Run the fused K-split reduce-scatter of ``len(a_slabs)`` ranks on ONE
     GPU: the same kernel, launched once per emulated rank in rank order, with
     the owners' slots / counters / outputs as local buffers.  No launch waits
     for another (the last contributor of each tile does the reduction), so
-    this is exactly the multi-GPU computation, serialised.  Returns the full
-    M x N output (the owners' slabs stacked)."""
+    this is exactly the multi-GPU computation, serialised.  In deferred mode
+    (the planner's default) the launches only deliver, and each owner's
+    bgx_rs_reduce then runs once, as it would after the barrier.  Returns the
+    full M x N output (the owners' slabs stacked)."""
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
     world = len(a_slabs)
@@ -281,6 +318,8 @@ def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> 
     pl = _lib.BgxRsPlan()
     _lib.check(lib.bgx_contract_rs_plan(d, world, pl), "bgx_contract_rs_plan")
     M, N, rpo = p.M, p.N, pl.rows_per_owner
+    kb = min(-(-_rs_desc(spec, a, b, out_dtype)[1].K // _BK) for a, b in zip(a_slabs, b_slabs))
+    _finish_plan(pl, M, N, min(local_splits or pl.local_splits, kb), mode)
     dev = a_slabs[0].device
     slots = torch.empty(world, pl.slot_bytes // 4, dtype=torch.float32, device=dev)
     counters = torch.zeros(world, max(4, pl.counter_bytes // 4), dtype=torch.int32, device=dev)
@@ -295,7 +334,7 @@ def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> 
         rs.counters[r] = counters[r].data_ptr()
         rs.out[r] = out[r * rpo].data_ptr()
         rs.c0[r] = c0_pad[r * rpo].data_ptr() if c0_pad is not None else None
-    if pl.local_splits > 1:
+    if pl.ws_bytes > 0:
         ws = torch.empty(pl.ws_bytes, dtype=torch.uint8, device=dev)
         wsc = torch.zeros(max(16, pl.counter_bytes), dtype=torch.uint8, device=dev)
         rs.ws, rs.ws_counters = ws.data_ptr(), wsc.data_ptr()
@@ -308,6 +347,12 @@ def emulate_fused_ksplit(spec, a_slabs, b_slabs, *, c0=None, out_dtype=None) -> 
         rs.plan = pl
         _lib.check(lib.bgx_contract_reduce_scatter(dr, rs, stream), "bgx_contract_reduce_scatter")
         executor._log("tcgen05-rs")
+    if pl.mode == _lib.RS_DEFERRED:
+        for r in range(world):
+            pl.rank = r
+            rs.plan = pl
+            _lib.check(lib.bgx_rs_reduce(d, rs, stream), "bgx_rs_reduce")
+            executor._log("rs-reduce")
     return out[:M]
 
 

@@ -1,0 +1,4 @@
+#!/bin/bash
+python -m pytest tests/test_gpu_fused_ksplit.py -x -q 2>&1 | tail -2
+python scripts/rs_probe.py 2>&1 | tail -3
+python scripts/rs_world1_probe.py 2>&1 | head -2

@@ -10,7 +10,7 @@ import socket
 import pytest
 import torch
 
-from paper_2503_04771_b200 import executor, shard
+from paper_2503_04771_b200 import _lib, executor, shard
 
 pytestmark = pytest.mark.gpu
 MM = "(i,k),(k,j)->(i,j)"
@@ -37,7 +37,8 @@ def test_emulated_reduce_scatter_matches(dev, world, M, N, K):
     A, B = _slabs(a, b, world)
     executor.reset_launch_log()
     out = shard.emulate_fused_ksplit(MM, A, B)
-    assert executor.launch_log() == ["tcgen05-rs"] * world
+    # default (deferred) mode: world delivering GEMMs, then each owner's reduce
+    assert executor.launch_log() == ["tcgen05-rs"] * world + ["rs-reduce"] * world
     assert out.shape == (M, N) and out.dtype == torch.bfloat16
     assert _relf(out, want) < 1e-2
     again = shard.emulate_fused_ksplit(MM, A, B)
@@ -65,7 +66,42 @@ def test_plan_tiles_and_ownership(dev):
     assert (pl.cta_group, pl.rows_per_owner) == (2, 128)
     pl2 = shard.rs_plan(MM, torch.empty(4096, 2048, device=dev, dtype=torch.bfloat16), b, 2)
     assert (pl2.cta_group, pl2.tile_n, pl2.rows_per_owner) == (2, 256, 2048)
-    assert pl.local_splits >= 1 and pl.slot_bytes == 8 * 128 * 1024 * 4
+    assert pl.mode == _lib.RS_DEFERRED and pl.ws_bytes == 0
+    assert pl.local_splits >= 1 and pl.slot_bytes == 8 * pl.local_splits * 128 * 1024 * 4
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("splits", [None, 1, 3])
+def test_deferred_and_in_kernel_modes_bit_identical(dev, world, splits):
+    """Both reduction placements sum the same partials in the same order
+    (slices inside a rank, ranks in rank order, then c0): identical bits,
+    with ragged K slabs, c0 and a forced local split."""
+    M, N, K = 640, 384, 6144 + 64 * world
+    g = torch.Generator(device=dev).manual_seed(world * 7 + (splits or 0))
+    a = torch.randn(M, K, device=dev, generator=g).bfloat16()
+    b = torch.randn(K, N, device=dev, generator=g).bfloat16()
+    c0 = torch.randn(M, N, device=dev, generator=g).bfloat16()
+    ks = {1: [(0, K)], 2: [(0, 2048), (2048, K)],
+          3: [(0, 1024), (1024, 4096), (4096, K)]}.get(world)     # ragged K slabs
+    A, B = _slabs(a, b, world, ks)
+    outs = [shard.emulate_fused_ksplit(MM, A, B, c0=c0, mode=m, local_splits=splits)
+            for m in (_lib.RS_IN_KERNEL, _lib.RS_DEFERRED)]
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    assert _relf(outs[1], a.double() @ b.double() + c0.double()) < 1e-2
+
+
+def test_deferred_rejects_split_beyond_k_blocks(dev):
+    a = torch.randn(256, 128, device=dev).bfloat16()     # 2 k-blocks
+    b = torch.randn(128, 256, device=dev).bfloat16()
+    d, _ = shard._rs_desc(MM, a, b, torch.bfloat16)
+    pl = shard.rs_plan(MM, a, b, 1)
+    shard._finish_plan(pl, 256, 256, 4, _lib.RS_DEFERRED)
+    rs = _lib.BgxReduceScatter()
+    buf = torch.zeros(pl.slot_bytes + 4096, dtype=torch.uint8, device=dev)
+    rs.plan, rs.slots[0], rs.counters[0], rs.out[0] = pl, buf.data_ptr(), buf.data_ptr(), buf.data_ptr()
+    lib = _lib.load()
+    assert lib.bgx_contract_reduce_scatter(d, rs, None) == _lib.ERR_INVALID
+    assert b"k-blocks" in lib.bgx_last_error()
 
 
 def test_transposed_operands(dev):
