@@ -103,3 +103,19 @@ def test_umma_descriptor_encodings(probe):
     assert probe["sdesc"] == [sdesc(0x12400, 16, 1024), sdesc(0x3F800, 8192, 1024)]
     assert probe["idesc"] == [idesc(1, 0, 1, 128, 256), idesc(0, 1, 0, 128, 64),
                               idesc(1, 1, 1, 256, 128)]
+
+
+def test_rs_plan_sizes_follow_mode_and_split():
+    """shard._finish_plan: deferred slots hold world x local_splits partial
+    planes and need no local workspace; in-kernel slots hold one plane per
+    rank plus a local split workspace (bgx.h bgx_rs_plan)."""
+    from paper_2503_04771_b200 import shard
+    pl = _lib.BgxRsPlan()
+    pl.world, pl.rows_per_owner = 8, 128
+    shard._finish_plan(pl, 1024, 512, 4, _lib.RS_DEFERRED)
+    assert (pl.mode, pl.local_splits, pl.ws_bytes) == (_lib.RS_DEFERRED, 4, 0)
+    assert pl.slot_bytes == 8 * 4 * 128 * 512 * 4
+    shard._finish_plan(pl, 1024, 512, 3, _lib.RS_IN_KERNEL)
+    assert pl.slot_bytes == 8 * 128 * 512 * 4 and pl.ws_bytes == 3 * 1024 * 512 * 4
+    shard._finish_plan(pl, 1024, 512, 0, None)          # clamps to one slice
+    assert pl.local_splits == 1 and pl.ws_bytes == 0
