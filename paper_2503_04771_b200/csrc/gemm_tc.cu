@@ -608,7 +608,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         }
         tmem_ld_wait();
         arrive_empty(acc);
-        if (p.rs_defer) continue;   // delivered; the owner's bgx_rs_reduce sums
+        if (p.rs_defer) {
+          // delivered; the owner's bgx_rs_reduce sums after the caller's
+          // barrier — make this thread's peer stores visible system-wide
+          // before the kernel can be seen as finished
+          __threadfence_system();
+          continue;
+        }
         // a CTA half entirely below the last output row has no owner (its
         // rows do not exist): nothing to deliver, no counter to bump
         if (tm * C::TILE_M + rank * BM >= p.M) continue;
