@@ -195,3 +195,28 @@ def test_fused_reduce_scatter_fuzz(dev):
         torch.cuda.synchronize()
         want = a.double() @ b.double() + (c0.double() if c0 is not None else 0)
         assert _relf(y, want) < 1e-2, (it, world, M, N, out_dt)
+
+
+def test_ksplit_demo_size_world8(dev):
+    """SURVEY §8e K-split demo at full size (1024 x 1024, K = 2^21 over 8
+    emulated ranks): f64 row samples, exact scaling by 2, both reduction
+    placements bit-identical."""
+    import numpy as np
+
+    import oracle
+    M = N = 1024
+    K = 1 << 21
+    g = torch.Generator(device=dev).manual_seed(21)
+    a = torch.randn(M, K, device=dev, generator=g).bfloat16()
+    b = torch.randn(K, N, device=dev, generator=g).bfloat16()
+    A, B = _slabs(a, b, 8)
+    out = shard.emulate_fused_ksplit(MM, A, B)
+    rows = np.random.default_rng(4).choice(M, 4, replace=False)
+    ar = a[torch.as_tensor(rows, device=dev)].double()
+    want = (ar @ b.double()).cpu().numpy()
+    got = out[torch.as_tensor(rows, device=dev)].float().cpu().numpy()
+    assert oracle.rel_frobenius(got, want) <= 1e-2
+    twice = shard.emulate_fused_ksplit(MM, [x * 2 for x in A], B)
+    assert torch.equal(twice, out * 2)
+    ink = shard.emulate_fused_ksplit(MM, A, B, mode=_lib.RS_IN_KERNEL)
+    assert torch.equal(ink.view(torch.int16), out.view(torch.int16))
