@@ -362,11 +362,83 @@ def run_chain(p: ChainPlan, spec: EinsumSpec, inputs, c0, out, *, mode, schedule
     return out
 
 
+def _exec_key(spec, inputs, c0, out, mode, chain_order):
+    """Everything a plain GEMM launch decision depends on (shapes, strides,
+    dtypes, devices, 16-byte alignment of every pointer, mode)."""
+    parts = [spec, mode, chain_order, out.dtype, out.device,
+             (out.shape, out.stride(), out.data_ptr() % 16)]
+    for t in inputs:
+        parts.append((t.shape, t.stride(), t.dtype, t.device, t.data_ptr() % 16))
+    parts.append(None if c0 is None else
+                 (c0.shape, c0.stride(), c0.dtype, c0.device, c0.data_ptr() % 16))
+    return tuple(parts)
+
+
+def _exec_cache() -> dict:
+    if not hasattr(_trace, "exec_cache"):
+        _trace.exec_cache = {}
+    return _trace.exec_cache
+
+
+def _fast_gemm(plan, spec, inputs, c0, out, mode):
+    """Pre-built descriptor for a plain GEMM (no operand copy, no output
+    permute, no split-K workspace, no padding): later calls with the same
+    signature patch the pointers and call bgx_contract directly — what
+    ``prepare()`` does, applied automatically to repeated ``execute`` calls
+    (the reference-shaped ``run_function`` path of BASELINE config 1)."""
+    if plan.a_view.needs_copy or plan.b_view.needs_copy or mode == "tf32":
+        return None
+    ext = extents_of(spec, [t.shape for t in inputs] + [out.shape])
+    so = _group_strides(out, spec.output, plan.o_view.axes, ext)
+    sc = (0, 0, 0) if c0 is None else _group_strides(c0, spec.output, plan.o_view.axes, ext)
+    if any(x is None for x in (*so, *sc)):
+        return None
+    ia, ib = plan.a, plan.b
+    sa = _group_strides(inputs[ia], spec.inputs[ia], plan.a_view.axes, ext)
+    sb = _group_strides(inputs[ib], spec.inputs[ib], plan.b_view.axes, ext)
+    lib = _lib.load()
+    d = _lib.BgxContractDesc()
+    d.batch, d.M, d.N, d.K = plan.batch, plan.M, plan.N, plan.K
+    for i in range(3):
+        d.a_stride[i], d.b_stride[i], d.c_stride[i], d.o_stride[i] = sa[i], sb[i], sc[i], so[i]
+    d.in_dtype = TORCH_TO_BGX[inputs[0].dtype]
+    d.out_dtype = TORCH_TO_BGX[out.dtype]
+    d.mode = MODES[mode]
+    d.a, d.b, d.out = inputs[ia].data_ptr(), inputs[ib].data_ptr(), out.data_ptr()
+    d.c0 = c0.data_ptr() if c0 is not None else None
+    kind = lib.bgx_contract_kernel(d)
+    if kind < 0 or (kind == _lib.KERNEL_SIMT16 and mode == "auto"
+                    and 2 * plan.batch * plan.M * plan.N * plan.K >= PAD_MIN_FLOP):
+        return None
+    if kind == _lib.KERNEL_TC:
+        sp, ws = _lib._i32(1), _lib._i64(0)
+        _lib.check(lib.bgx_contract_splitk_plan(d, sp, ws), "bgx_contract_splitk_plan")
+        if sp.value != 1:
+            return None
+    name = _lib.KERNEL_NAMES.get(kind, "contract")
+
+    def run(xs, o, c):
+        d.a, d.b, d.out = xs[ia].data_ptr(), xs[ib].data_ptr(), o.data_ptr()
+        d.c0 = c.data_ptr() if c is not None else None
+        with _on_device(o.device):
+            _lib.check(lib.bgx_contract(d, _stream_ptr(o)), "bgx_contract")
+        _log(name)
+    return run
+
+
 def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
             mode: str = "auto", schedule=None, chain_order: str = "left"):
     """Run one generic op into ``out`` (fresh, contiguous-or-strided device
     tensor).  ``c0`` is the initial output (None = zeros); ignored by a
     passthrough body, exactly as in the reference (einsum.py:105-108)."""
+    key = None
+    if schedule is None and all(isinstance(t, torch.Tensor) and t.is_cuda for t in inputs) \
+            and out.is_cuda and (c0 is None or c0.is_cuda):
+        key = _exec_key(spec, inputs, c0, out, mode, chain_order)
+        fast = _exec_cache().get(key)
+        if fast is not None:
+            fast(inputs, out, c0)
+            return out
     _check_device(list(inputs) + [c0, out])
     dt = out.dtype
     for t in inputs:
@@ -385,7 +457,15 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
         generic(spec, inputs, c0, tmp)
         return permute(tmp, out, list(range(out.dim())))
     if isinstance(plan, GemmPlan):
-        return run_gemm(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)
+        run_gemm(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)
+        if key is not None and dt == inputs[0].dtype:
+            fast = _fast_gemm(plan, spec, inputs, c0, out, mode)
+            if fast is not None:
+                cache = _exec_cache()
+                if len(cache) > 256:
+                    cache.clear()
+                cache[key] = fast
+        return out
     if isinstance(plan, ChainPlan):
         return run_chain(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)
     raise AssertionError(plan)
