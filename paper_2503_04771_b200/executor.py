@@ -380,12 +380,13 @@ def _exec_cache() -> dict:
     return _trace.exec_cache
 
 
-def _fast_gemm(plan, spec, inputs, c0, out, mode):
+def _fast_gemm(plan, spec, inputs, c0, out, mode, log: bool = True):
     """Pre-built descriptor for a plain GEMM (no operand copy, no output
     permute, no split-K workspace, no padding): later calls with the same
     signature patch the pointers and call bgx_contract directly — what
-    ``prepare()`` does, applied automatically to repeated ``execute`` calls
-    (the reference-shaped ``run_function`` path of BASELINE config 1)."""
+    ``prepare()`` does (it builds its GEMM launcher here too), applied
+    automatically to repeated ``execute`` calls (the reference-shaped
+    ``run_function`` path of BASELINE config 1)."""
     if plan.a_view.needs_copy or plan.b_view.needs_copy or mode == "tf32":
         return None
     ext = extents_of(spec, [t.shape for t in inputs] + [out.shape])
@@ -422,7 +423,8 @@ def _fast_gemm(plan, spec, inputs, c0, out, mode):
         d.c0 = c.data_ptr() if c is not None else None
         with _on_device(o.device):
             _lib.check(lib.bgx_contract(d, _stream_ptr(o)), "bgx_contract")
-        _log(name)
+        if log:
+            _log(name)
     return run
 
 

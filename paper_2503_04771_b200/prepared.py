@@ -85,38 +85,15 @@ class Prepared:
                 d.out = o.data_ptr()
                 return self._lib.bgx_generic(d, torch.cuda.current_stream().cuda_stream)
             return run
-        if isinstance(p, GemmPlan) and not (p.a_view.needs_copy or p.b_view.needs_copy):
-            ext = extents_of(spec, [t.shape for t in ins] + [out.shape])
-            so = executor._group_strides(out, spec.output, p.o_view.axes, ext)
-            sc = (0, 0, 0)
-            if self.c0 is not None:
-                sc = executor._group_strides(self.c0, spec.output, p.o_view.axes, ext)
-            if any(x is None for x in (*so, *sc)) or self.mode == "tf32":
+        if isinstance(p, GemmPlan) and not self.schedule:
+            run = executor._fast_gemm(p, spec, ins, self.c0, out, self.mode, log=False)
+            if run is None:
                 return None
-            sa = executor._group_strides(ins[p.a], spec.inputs[p.a], p.a_view.axes, ext)
-            sb = executor._group_strides(ins[p.b], spec.inputs[p.b], p.b_view.axes, ext)
-            d = _lib.BgxContractDesc()
-            d.batch, d.M, d.N, d.K = p.batch, p.M, p.N, p.K
-            for i in range(3):
-                d.a_stride[i], d.b_stride[i], d.c_stride[i], d.o_stride[i] = sa[i], sb[i], sc[i], so[i]
-            d.in_dtype = executor.TORCH_TO_BGX[ins[0].dtype]
-            d.out_dtype = executor.TORCH_TO_BGX[out.dtype]
-            d.mode = executor.MODES[self.mode]
-            d.a, d.b, d.out = ins[p.a].data_ptr(), ins[p.b].data_ptr(), out.data_ptr()
-            d.c0 = self.c0.data_ptr() if self.c0 is not None else None
-            kind = self._lib.bgx_contract_kernel(d)
-            sp, ws = _lib._i32(1), _lib._i64(0)
-            if kind == _lib.KERNEL_TC:
-                self._lib.bgx_contract_splitk_plan(d, sp, ws)
-            if kind < 0 or sp.value > 1 or self.schedule:
-                return None
-            ia, ib = p.a, p.b
 
-            def run(xs, o, c0):
-                d.a, d.b, d.out = xs[ia].data_ptr(), xs[ib].data_ptr(), o.data_ptr()
-                d.c0 = c0.data_ptr() if c0 is not None else None
-                return self._lib.bgx_contract(d, torch.cuda.current_stream().cuda_stream)
-            return run
+            def fast(xs, o, c0):
+                run(xs, o, c0)
+                return 0
+            return fast
         return None
 
     def _launch(self, xs, o, c0):
