@@ -210,9 +210,12 @@ class FusedKSplit:
 
     def __init__(self, spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *, out_dtype=None,
                  group=None, with_c0: bool = False, local_splits: int | None = None,
-                 mode: int | None = None):
+                 mode: int | None = None, barrier_timeout_ms: int = 60000):
         self.spec = spec if isinstance(spec, EinsumSpec) else parse_einsum(spec)
         self.group = group
+        # device barriers give up (a CUDA error, not a hang) if a peer never
+        # arrives — e.g. a rank that failed between two calls
+        self.barrier_timeout_ms = int(barrier_timeout_ms)
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.out_dtype = out_dtype or a_slab.dtype
@@ -250,7 +253,7 @@ class FusedKSplit:
             self.buf[offs["counters"]:offs["counters"] + pl.counter_bytes].zero_()
             self.hdl = symm_mem.rendezvous(self.buf, self.group or dist.group.WORLD)
             bases = list(self.hdl.buffer_ptrs)
-            self.hdl.barrier()
+            self.hdl.barrier(0, self.barrier_timeout_ms)
         else:
             self.buf = torch.zeros(total, dtype=torch.uint8, device=self.dev)
             self.hdl = None
@@ -286,13 +289,13 @@ class FusedKSplit:
         self.desc.a = ins[self._a_idx].data_ptr()
         self.desc.b = ins[1 - self._a_idx].data_ptr()
         if self.hdl is not None:
-            self.hdl.barrier()
+            self.hdl.barrier(0, self.barrier_timeout_ms)
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         _lib.check(self._lib.bgx_contract_reduce_scatter(self.desc, self.rs, stream),
                    "bgx_contract_reduce_scatter")
         executor._log("tcgen05-rs")
         if self.hdl is not None:
-            self.hdl.barrier()
+            self.hdl.barrier(0, self.barrier_timeout_ms)
         if self.plan.mode == _lib.RS_DEFERRED:   # every partial of my rows is in my slots
             _lib.check(self._lib.bgx_rs_reduce(self.desc, self.rs, stream), "bgx_rs_reduce")
             executor._log("rs-reduce")
