@@ -486,11 +486,13 @@ int launch(const bgx_contract_desc &d, cudaStream_t s) {
     int64_t blocks = p.tiles_m * p.tiles_n * d.batch;
     if (blocks > 0x7fffffffLL) { set_error("simt gemm: grid too large"); return BGX_ERR_UNSUPPORTED; }
     // f32 row-major operands (A K-major, B N-major, 16-byte rows): cp.async pipeline
+    // (BGX_NO_SIMT_CP, read once per process: the register-staged kernel, for A/B)
+    static const bool no_cp = getenv("BGX_NO_SIMT_CP") != nullptr;
     const bool cp_ok = std::is_same<In, float>::value && std::is_same<Out, float>::value &&
                        d.a_stride[2] == 1 && d.b_stride[2] == 1 && d.a_stride[1] % 4 == 0 &&
                        d.b_stride[1] % 4 == 0 && (d.batch <= 1 || (d.a_stride[0] % 4 == 0 &&
                        d.b_stride[0] % 4 == 0)) && ((uintptr_t)d.a % 16) == 0 &&
-                       ((uintptr_t)d.b % 16) == 0 && !getenv("BGX_NO_SIMT_CP");
+                       ((uintptr_t)d.b % 16) == 0 && !no_cp;
     // 2 stages: a third (measured, 55 KB dynamic smem) was 2-3% slower
     if (cp_ok) simt_f32_cp_kernel<FUSED, 2><<<(unsigned)blocks, 256, cp_smem_bytes<2>(), s>>>(p);
     else simt_gemm_big_kernel<In, Out, Acc, FUSED><<<(unsigned)blocks, 256, 0, s>>>(p);
