@@ -139,3 +139,31 @@ def test_concurrent_threads_and_streams(dev):
     for t in threads:
         t.join()
     assert not errors, errors[:3]
+
+
+def test_execute_launch_cache_matches_uncached(dev):
+    """The per-signature GEMM launch cache (executor._fast_gemm): repeated
+    calls, views at other offsets (different 16-byte alignment), c0 on/off,
+    f32 exact and bf16 tensor-core plans — identical results and launch-log
+    names to the uncached path."""
+    from paper_2503_04771_b200 import executor
+    g = torch.Generator(device=dev).manual_seed(3)
+    base = torch.randn(300 * 130 + 64, device=dev, generator=g)
+    b = torch.randn(128, 96, device=dev, generator=g)
+    c0 = torch.randn(300, 96, device=dev, generator=g)
+    spec = "(i,k),(k,j)->(i,j)"
+    for dt in (torch.float32, torch.bfloat16):
+        for off in (0, 1, 4, 0, 1):           # revisit signatures: cache hits
+            a = base[off:off + 300 * 128].view(300, 128).to(dt)
+            if off % 4:                        # misaligned view of the same shape
+                a = base.to(dt)[off:off + 300 * 128].view(300, 128)
+            for c in (None, c0.to(dt)):
+                executor._exec_cache().clear()
+                executor.reset_launch_log()
+                want = contract(spec, a, b.to(dt), c0=c)
+                first = executor.launch_log()
+                executor.reset_launch_log()
+                got1 = contract(spec, a, b.to(dt), c0=c)     # builds the cache entry
+                got2 = contract(spec, a, b.to(dt), c0=c)     # cached launch
+                assert torch.equal(got1, want) and torch.equal(got2, want)
+                assert executor.launch_log() == first * 2
