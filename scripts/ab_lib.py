@@ -29,8 +29,9 @@ SHAPES = {"c4_4096": (1, 4096, 4096, 4096), "c3_b64_1024": (64, 1024, 1024, 1024
 def load(path):
     lib = ctypes.CDLL(os.path.abspath(path))
     for name, (res, args) in _lib.SIGNATURES.items():
-        fn = getattr(lib, name)
-        fn.restype, fn.argtypes = res, args
+        fn = getattr(lib, name, None)   # an older build may lack newer entry points
+        if fn is not None:
+            fn.restype, fn.argtypes = res, args
     return lib
 
 
