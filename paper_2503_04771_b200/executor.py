@@ -57,8 +57,14 @@ def _log(name: str):
     launch_log().append(name)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_ptr(t: torch.Tensor):
-    """cudaStream_t of torch's current stream on ``t``'s device (as int)."""
+    """cudaStream_t of torch's current stream on ``t``'s device (as int);
+    the raw getter skips building a torch.cuda.Stream object per launch."""
+    if _raw_stream is not None and t.device.index is not None:
+        return _raw_stream(t.device.index)
     return torch.cuda.current_stream(t.device).cuda_stream
 
 

@@ -71,7 +71,8 @@ class TensorValue:
             want = _TORCH[self.elem]
             if self.data.dtype != want:
                 raise InterpError(f"tensor dtype {self.data.dtype} does not match {self.elem}")
-            self.data = self.data.reshape(tuple(self.dims))
+            if tuple(self.data.shape) != tuple(self.dims):
+                self.data = self.data.reshape(tuple(self.dims))
         else:
             npd = _NP.get(self.elem) or _np_bf16()
             if npd is None:
