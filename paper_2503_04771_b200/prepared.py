@@ -6,7 +6,8 @@ repeated contractions of the same shapes/layouts.  ``prepare`` parses the
 spec, classifies it and builds the C descriptor (``bgx_contract_desc`` /
 ``bgx_tensor`` / ``bgx_generic_desc``) once; each call only patches the data
 pointers and calls the C ABI — a few microseconds of host time instead of the
-~65 us of the general ``contract`` path.  With ``graph=True`` the launch(es)
+15-30 us of the general ``contract`` path (which itself reuses a cached
+descriptor for a repeated GEMM signature).  With ``graph=True`` the launch(es)
 are captured into a CUDA graph over the example tensors (which become the
 static buffers: copy new data into ``.inputs`` / read ``.out``) and each call
 is one ``cudaGraphLaunch``.  Plans that need a permute pre-pass, a chain of
