@@ -23,6 +23,7 @@ SSA values of multi-generic functions never leave it.
 from __future__ import annotations
 
 from dataclasses import dataclass
+import threading
 
 import numpy as np
 import torch
@@ -105,12 +106,52 @@ def _to_host(t: torch.Tensor, elem: ElemType) -> np.ndarray:
     return t.cpu().numpy()
 
 
+_replay = threading.local()
+
+
+def _replay_key(module, symbol, inputs, mode, device, schedule):
+    """Signature of a device-resident call (None when the call does not
+    qualify): everything the interpreter's checks and plans depend on."""
+    sig = []
+    for v in inputs:
+        if type(v) is not TensorValue or not isinstance(v.data, torch.Tensor) or not v.data.is_cuda:
+            return None
+        sig.append((v.elem, v.dims, v.data.device))
+    sk = schedule if schedule is None or isinstance(schedule, str) else repr(schedule)
+    return (id(module), symbol, mode, device, sk, tuple(sig))
+
+
 def run_function(module: Module, symbol: str, inputs, step_limit=DEFAULT_STEP_LIMIT,
                  thread_ctx=None, *, mode: str = "auto", device=None, schedule=None):
     """Execute ``@symbol`` on ``inputs`` (list of TensorValue); returns the
     list of result TensorValues.  ``mode`` selects the kernel class for
     contractions ('auto', 'exact', 'ffma', 'tc', 'simt' — see bgx.h);
-    'auto' is bit-exact with the reference for f32/f64 inputs."""
+    'auto' is bit-exact with the reference for f32/f64 inputs.
+
+    A device-resident call whose signature (module, symbol, element types,
+    shapes, devices, mode, schedule) already ran to completion replays the
+    recorded op sequence without re-deriving extents and step counts — the
+    checks would pass again and the step count is a function of the shapes,
+    so the replay is taken only when that count fits ``step_limit``."""
+    inputs = list(inputs)
+    key = _replay_key(module, symbol, inputs, mode, device, schedule)
+    cache = getattr(_replay, "d", None)
+    if cache is None:
+        cache = _replay.d = {}
+    if key is not None:
+        hit = cache.get(key)
+        if hit is not None and hit[0] is module and (step_limit is None or hit[1] <= step_limit):
+            return hit[2](inputs)
+    results, steps, replay = _run_function(module, symbol, inputs, step_limit, mode, device,
+                                           schedule)
+    if key is not None and replay is not None:
+        if len(cache) > 64:
+            cache.clear()
+        cache[key] = (module, steps, replay)
+    return results
+
+
+def _run_function(module, symbol, inputs, step_limit, mode, device, schedule):
     fn = module.lookup_symbol(symbol)
     if fn is None:
         raise InterpError(f"no function @{symbol} in the module")
@@ -128,6 +169,7 @@ def run_function(module: Module, symbol: str, inputs, step_limit=DEFAULT_STEP_LI
     env = {id(a): v for a, v in zip(fn.arguments, inputs)}
     dev = {}
     steps = 0
+    plan = []
 
     def tick(n=1):
         nonlocal steps
@@ -169,6 +211,7 @@ def run_function(module: Module, symbol: str, inputs, step_limit=DEFAULT_STEP_LI
         res = op.results[0]
         env[id(res)] = TensorValue(op.elem, tuple(out_t.shape), out_t)
         dev[id(res)] = out_t
+        plan.append((op, tuple(vals[-1].dims), _TORCH[op.elem], sched))
     tick()  # func.return
     results = []
     for v in fn.returns:
@@ -176,4 +219,21 @@ def run_function(module: Module, symbol: str, inputs, step_limit=DEFAULT_STEP_LI
         if host_io and isinstance(tv.data, torch.Tensor):
             tv = TensorValue(tv.elem, tv.dims, _to_host(tv.data, tv.elem))
         results.append(tv)
-    return results
+    replay = None
+    if not host_io:
+        args, rets = fn.arguments, fn.returns
+
+        def replay(new_inputs):
+            env2 = {id(a): v.data for a, v in zip(args, new_inputs)}
+            with executor._on_device(device):
+                for op, dims, dtype, sch in plan:
+                    ts = [env2[id(x)] for x in op.operands]
+                    o = torch.empty(dims, dtype=dtype, device=device)
+                    executor.execute(op.spec, ts[:-1], ts[-1], o, mode=mode, schedule=sch)
+                    env2[id(op.results[0])] = o
+            return [TensorValue(elem_of[id(v)], tuple(env2[id(v)].shape), env2[id(v)])
+                    for v in rets]
+        elem_of = {id(v): env[id(v)].elem for v in rets}
+        if not all(isinstance(env[id(v)].data, torch.Tensor) for v in rets):
+            replay = None
+    return results, steps, replay
