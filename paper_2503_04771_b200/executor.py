@@ -434,6 +434,24 @@ def _fast_gemm(plan, spec, inputs, c0, out, mode, log: bool = True):
     return run
 
 
+def _fast_permute(x, out, perm):
+    """Pre-built bgx_tensor pair for a repeated permutation signature."""
+    lib = _lib.load()
+    ti, to = _lib.BgxTensor(), _lib.BgxTensor()
+    for t, desc in ((x, ti), (out, to)):
+        desc.dtype, desc.rank = TORCH_TO_BGX[t.dtype], t.dim()
+        for d in range(t.dim()):
+            desc.shape[d], desc.stride[d] = t.shape[d], t.stride(d)
+    p = (_lib._i32 * max(1, len(perm)))(*perm)
+
+    def run(xs, o, c):
+        ti.data, to.data = xs[0].data_ptr(), o.data_ptr()
+        with _on_device(o.device):
+            _lib.check(lib.bgx_permute(ti, to, p, _stream_ptr(o)), "bgx_permute")
+        _log("permute")
+    return run
+
+
 def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
             mode: str = "auto", schedule=None, chain_order: str = "left"):
     """Run one generic op into ``out`` (fresh, contiguous-or-strided device
@@ -457,7 +475,10 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     plan = plan_generic(spec, shapes, strides, dtype=DTYPE_NAME[dt], mode=mode,
                         chain_order=chain_order)
     if isinstance(plan, PermutePlan):
-        return permute(inputs[0], out, plan.perm)
+        permute(inputs[0], out, plan.perm)
+        if key is not None:
+            _exec_cache()[key] = _fast_permute(inputs[0], out, plan.perm)
+        return out
     if isinstance(plan, GenericPlan):
         if out.is_contiguous():
             return generic(spec, inputs, c0, out)

@@ -167,3 +167,20 @@ def test_execute_launch_cache_matches_uncached(dev):
                 got2 = contract(spec, a, b.to(dt), c0=c)     # cached launch
                 assert torch.equal(got1, want) and torch.equal(got2, want)
                 assert executor.launch_log() == first * 2
+
+
+@pytest.mark.parametrize("spec,shape", [("(i,j)->(j,i)", (300, 257)), ("(i,j,k)->(k,j,i)", (7, 9, 33)),
+                                        ("(i,j)->(i,j)", (64, 64))])
+def test_execute_launch_cache_permutations(dev, spec, shape):
+    """Cached permutation launches: bit-exact, including strided views."""
+    from paper_2503_04771_b200 import executor
+    from paper_2503_04771_b200.einsum import parse_einsum
+    sp = parse_einsum(spec)
+    perm = [sp.inputs[0].index(ax) for ax in sp.output]
+    base = torch.randn((shape[0] * 2,) + tuple(shape[1:]), device=dev)
+    for x in (base[: shape[0]], base[::2], base[: shape[0]]):
+        executor.reset_launch_log()
+        for _ in range(3):
+            y = contract(spec, x)
+            assert torch.equal(y, x.permute(perm).contiguous())
+        assert executor.launch_log() == ["permute"] * 3
