@@ -84,3 +84,29 @@ def fullsize_c1():
 def sha256(a) -> str:
     import hashlib
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def import_bridgegen():
+    """Import the REAL reference package for the drop-in tests.
+
+    On the GPU box the reference tree is absent; ``__graft_entry__.build()``
+    pip-installs it (pure Python, ``--no-deps``) into the git-ignored
+    ``baseline/_ref``, which travels with the snapshot.  Here (build
+    container) ``/root/reference/pkg/src`` is used when the install is
+    missing.  A missing package is a hard error, never a skip: a green GPU
+    run must not hide zero coverage of the plug-in path."""
+    import importlib
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for cand in (os.path.join(root, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(cand, "bridgegen")):
+            if cand not in sys.path:
+                sys.path.append(cand)
+            break
+    try:
+        return importlib.import_module("bridgegen")
+    except ImportError as e:  # pragma: no cover - exercised only on a broken box
+        raise ImportError(
+            "bridgegen (the reference package) is not importable: run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` in the build "
+            "container so baseline/_ref ships with the snapshot") from e

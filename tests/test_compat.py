@@ -18,12 +18,7 @@ import pytest
 import _golden as G
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-for cand in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
-    if os.path.isdir(os.path.join(cand, "bridgegen")) and cand not in sys.path:
-        sys.path.append(cand)
-        break
-
-bridgegen = pytest.importorskip("bridgegen")
+bridgegen = G.import_bridgegen()   # hard failure, never a skip
 from bridgegen import einsum, interp, intrinsics, ir  # noqa: E402
 from bridgegen.gpu import register_gpu_intrinsics  # noqa: E402
 
