@@ -13,10 +13,11 @@ on top: element strides and dtype.  Output is one of
                otherwise the operand is first materialised in group order by
                a permute pre-pass (``needs_copy``);
   GenericPlan  anything else (single-input reductions, Hadamard / outer
-               products, A-only reduction axes, rank-0 outputs, 3+ inputs in
-               exact mode) → ``bgx_generic`` (the reference's loop nest on the
+               products, A-only reduction axes, rank-0 outputs, 3+ f32/f64 inputs in
+               'auto'/'exact' mode) → ``bgx_generic`` (the reference's loop nest on the
                device, bit-exact);
-  ChainPlan    3+ inputs evaluated as pairwise contractions (left-to-right or
+  ChainPlan    3+ 16-bit inputs (or any dtype in a non-exact mode) evaluated
+               as pairwise contractions (left-to-right or
                min-flop order) → a sequence of GemmPlans over intermediates.
 
 Everything here is host logic over integers — unit-tested on the CPU
@@ -34,8 +35,12 @@ from .einsum import EinsumSpec
 # group names
 BATCH, MGRP, NGRP, KGRP = "batch", "m", "n", "k"
 
-# exact-mode generic kernel is used for f32/f64 multi-operand specs up to
-# this many iteration points in AUTO mode; larger ones are planned pairwise.
+# f32/f64 multi-operand specs in 'auto' / 'exact' mode always run the
+# reference's unfactored loop nest (bit-exact, interp.py:407-420): pairwise
+# evaluation ((a*b) summed, then *c) changes the arithmetic, so it is only
+# planned for 16-bit operands or when the caller asks for a non-exact mode
+# ('tc', 'tf32', 'ffma', 'simt').  Above this many iteration points the
+# exact plan is still chosen but logged as slow (plan.kind says so).
 GENERIC_POINT_LIMIT = 1 << 28
 
 
@@ -188,8 +193,11 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
         return GenericPlan("single-input reduction")
     if n_in >= 3:
         points = _prod(ext[a] for a in spec.axes)
-        if ref_types and (mode == "exact" or points <= GENERIC_POINT_LIMIT):
-            return GenericPlan("multi-operand body, exact loop nest")
+        if ref_types and mode in ("auto", "exact"):
+            why = "multi-operand body, exact loop nest"
+            if points > GENERIC_POINT_LIMIT:
+                why += f" ({points} points: pass mode='tf32'/'ffma' for pairwise GEMMs)"
+            return GenericPlan(why)
         return plan_chain(spec, ext, order=chain_order)
     groups = classify_two(spec, ext)
     if isinstance(groups, str):

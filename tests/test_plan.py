@@ -83,3 +83,17 @@ def test_inconsistent_extent():
     spec = parse_einsum("(i,k),(k,j)->(i,j)")
     with pytest.raises(ValueError, match="inconsistent"):
         P.plan_generic(spec, [(4, 3), (2, 5), (4, 5)], [(3, 1), (5, 1), (5, 1)], dtype="f32")
+
+
+def test_reference_dtypes_stay_exact_at_any_size():
+    """'auto' on f32/f64 must keep the reference's unfactored loop
+    nest (bit-exact) however many points; pairwise chains only on request."""
+    ext = dict(i=1024, k=1024, j=1024, l=1024)   # 2^40 points > GENERIC_POINT_LIMIT
+    for dt in ("f32", "f64"):
+        for mode in ("auto", "exact"):
+            p = plan_of("(i,k),(k,j),(j,l)->(i,l)", ext, dtype=dt, mode=mode)
+            assert isinstance(p, P.GenericPlan) and "exact loop nest" in p.reason
+        for mode in ("tf32", "ffma"):
+            assert isinstance(plan_of("(i,k),(k,j),(j,l)->(i,l)", ext, dtype=dt, mode=mode),
+                              P.ChainPlan)
+    assert isinstance(plan_of("(i,k),(k,j),(j,l)->(i,l)", ext, dtype="bf16"), P.ChainPlan)
