@@ -57,6 +57,47 @@ def _log(name: str):
     launch_log().append(name)
 
 
+@contextlib.contextmanager
+def timed_launches():
+    """Record a CUDA event pair around every library launch this thread makes
+    (on the stream the kernel is launched on) while the context is open;
+    yields the list of ``(kernel_name, start_event, end_event)``.  Used by
+    bench.py to time the dominant kernel inside a public-API step."""
+    prev = getattr(_trace, "events", None)
+    _trace.events = []
+    try:
+        yield _trace.events
+    finally:
+        _trace.events = prev
+
+
+def _ev_begin(out):
+    evs = getattr(_trace, "events", None)
+    if evs is None:
+        return None
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record(torch.cuda.current_stream(out.device))
+    return e0
+
+
+def _ev_end(e0, name, out):
+    if e0 is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(torch.cuda.current_stream(out.device))
+        _trace.events.append((name, e0, e1))
+
+
+CACHE_LIMIT = 256
+
+
+def _cache_put(cache: dict, key, value, limit: int = CACHE_LIMIT):
+    """Insert into a per-thread launch cache, evicting the oldest entry once
+    ``limit`` entries are held (dicts keep insertion order)."""
+    if key not in cache and len(cache) >= limit:
+        cache.pop(next(iter(cache)))
+    cache[key] = value
+
+
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
@@ -233,10 +274,7 @@ def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, 
         tile = (cg.value, bn.value, splits.value)
         tile_log().append(tile)
     if key is not None:
-        cache = _launch_cache()
-        if len(cache) > 512:
-            cache.clear()
-        cache[key] = (d, kind, splits.value, ws_bytes.value, tile)
+        _cache_put(_launch_cache(), key, (d, kind, splits.value, ws_bytes.value, tile), 512)
     return _launch(lib, d, kind, splits.value, ws_bytes.value, out)
 
 
@@ -250,12 +288,18 @@ def _launch(lib, d, kind, splits, ws_bytes, out) -> int:
     with _on_device(out.device):
         if splits > 1 or splits < -1:
             ws = torch.empty(ws_bytes, dtype=torch.uint8, device=out.device)
+            name = "tcgen05-splitk" if splits > 1 else "tcgen05-tailsplit"
+            e0 = _ev_begin(out)
             _lib.check(lib.bgx_contract_splitk(d, splits, ws.data_ptr(), ws_bytes,
                                                _stream_ptr(out)), "bgx_contract_splitk")
-            _log("tcgen05-splitk" if splits > 1 else "tcgen05-tailsplit")
+            _ev_end(e0, name, out)
+            _log(name)
             return kind
+        name = _lib.KERNEL_NAMES.get(kind, "contract")
+        e0 = _ev_begin(out)
         _lib.check(lib.bgx_contract(d, _stream_ptr(out)), "bgx_contract")
-    _log(_lib.KERNEL_NAMES.get(kind, "contract"))
+        _ev_end(e0, name, out)
+    _log(name)
     return kind
 
 
@@ -428,7 +472,9 @@ def _fast_gemm(plan, spec, inputs, c0, out, mode, log: bool = True):
         d.a, d.b, d.out = xs[ia].data_ptr(), xs[ib].data_ptr(), o.data_ptr()
         d.c0 = c.data_ptr() if c is not None else None
         with _on_device(o.device):
+            e0 = _ev_begin(o)
             _lib.check(lib.bgx_contract(d, _stream_ptr(o)), "bgx_contract")
+            _ev_end(e0, name, o)
         if log:
             _log(name)
     return run
@@ -477,7 +523,7 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     if isinstance(plan, PermutePlan):
         permute(inputs[0], out, plan.perm)
         if key is not None:
-            _exec_cache()[key] = _fast_permute(inputs[0], out, plan.perm)
+            _cache_put(_exec_cache(), key, _fast_permute(inputs[0], out, plan.perm))
         return out
     if isinstance(plan, GenericPlan):
         if out.is_contiguous():
@@ -490,10 +536,7 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
         if key is not None and dt == inputs[0].dtype:
             fast = _fast_gemm(plan, spec, inputs, c0, out, mode)
             if fast is not None:
-                cache = _exec_cache()
-                if len(cache) > 256:
-                    cache.clear()
-                cache[key] = fast
+                _cache_put(_exec_cache(), key, fast)
         return out
     if isinstance(plan, ChainPlan):
         return run_chain(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)

@@ -137,9 +137,12 @@ def translate(func, kernel_name: str = "bgx_fir_kernel"):
 
     for blk in region.blocks:
         body.append(f"{labels[id(blk)]}: {{")
-        body.append(f"  steps += {len(blk.operations)};")
-        body.append("  if (steps > step_limit) { bgx_report(hdr, tab, key, 2, 0, 0, 0, 0); return; }")
         for op in blk.operations:
+            # tick, then execute (interp.py:231-233): a step-limit overrun
+            # and an out-of-bounds access in one block raise what the
+            # reference raises
+            body.append("  if (++steps > step_limit) "
+                        "{ bgx_report(hdr, tab, key, 2, 0, 0, 0, 0); return; }")
             name = op.name
             res = op.results[0] if op.results else None
             o = [var(x) for x in op.operands]
@@ -218,9 +221,12 @@ def translate(func, kernel_name: str = "bgx_fir_kernel"):
         f'extern "C" __global__ void {kernel_name}(' + ", ".join(
             params + ["unsigned long long* hdr", "ErrRec* tab", "i64 step_limit",
                       "unsigned long long total", "int reverse",
-                      "i64 gx", "i64 gy", "i64 gz", "i64 bx", "i64 by", "i64 bz"]) + ") {",
+                      "i64 gx", "i64 gy", "i64 gz", "i64 bx", "i64 by", "i64 bz",
+                      "unsigned long long only"]) + ") {",
         "  unsigned long long L = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;",
         "  if (L >= total) return;",
+        # re-run of the single first-failing coordinate (see run_kernel)
+        "  if (only != ~0ULL && (reverse ? total - 1 - L : L) != only) return;",
         # visiting order of interp.py:445-451: block x,y,z then thread x,y,z
         "  unsigned long long r = L;",
         "  i64 tz = r % bz; r /= bz; i64 ty = r % by; r /= by; i64 tx = r % bx; r /= bx;",
@@ -280,35 +286,52 @@ def run_kernel(module, symbol, launch, inputs, step_limit=None, reverse=False):
         raise interp.InterpError(str(e)) from e
     handle = _compile(src, "bgx_fir_kernel")
     dev = torch.device("cuda", torch.cuda.current_device())
-    keep, args = [], []
-    for v, kind in zip(inputs, kinds):
-        if kind[0] == "memref":
-            t = torch.from_numpy(np.ascontiguousarray(v.data)).to(dev)
-            keep.append(t)
-            args.append(ctypes.c_void_p(t.data_ptr()))
-            args += [ctypes.c_int64(int(e)) for e in v.data.shape]
-        else:
-            val = v.value
-            args.append(ctypes.c_float(val) if kind[1] == "float" else
-                        ctypes.c_double(val) if kind[1] == "double" else ctypes.c_int64(int(val)))
-    hdr = torch.tensor([0, (1 << 63) - 1], dtype=torch.int64, device=dev)
-    tab = torch.zeros((_ERR_SLOTS, 6), dtype=torch.int64, device=dev)
-    args += [ctypes.c_void_p(hdr.data_ptr()), ctypes.c_void_p(tab.data_ptr()),
-             ctypes.c_int64(int(step_limit)), ctypes.c_uint64(total),
-             ctypes.c_int32(1 if reverse else 0)] + [ctypes.c_int64(e) for e in (gx, gy, gz, bx, by, bz)]
-    argv = (ctypes.c_void_p * len(args))(*[ctypes.cast(ctypes.pointer(a), ctypes.c_void_p) for a in args])
-    block = 256
-    grid = (total + block - 1) // block
     lib = _lib.load()
     stream = torch.cuda.current_stream(dev).cuda_stream
-    _lib.check(lib.bgx_rtc_launch(handle, grid, block, argv, stream), "bgx_rtc_launch")
-    torch.cuda.synchronize(dev)
+
+    def launch(only):
+        """One launch over all coordinates (``only`` = -1) or over the single
+        coordinate whose visiting-order key is ``only``; fresh device copies
+        of the memrefs every time (returns them and the error header/table)."""
+        keep, args = [], []
+        for v, kind in zip(inputs, kinds):
+            if kind[0] == "memref":
+                t = torch.from_numpy(np.ascontiguousarray(v.data)).to(dev)
+                keep.append(t)
+                args.append(ctypes.c_void_p(t.data_ptr()))
+                args += [ctypes.c_int64(int(e)) for e in v.data.shape]
+            else:
+                val = v.value
+                args.append(ctypes.c_float(val) if kind[1] == "float" else
+                            ctypes.c_double(val) if kind[1] == "double" else ctypes.c_int64(int(val)))
+        hdr = torch.tensor([0, (1 << 63) - 1], dtype=torch.int64, device=dev)
+        tab = torch.zeros((_ERR_SLOTS, 6), dtype=torch.int64, device=dev)
+        args += [ctypes.c_void_p(hdr.data_ptr()), ctypes.c_void_p(tab.data_ptr()),
+                 ctypes.c_int64(int(step_limit)), ctypes.c_uint64(total),
+                 ctypes.c_int32(1 if reverse else 0)]
+        args += [ctypes.c_int64(e) for e in (gx, gy, gz, bx, by, bz)]
+        args.append(ctypes.c_uint64(only & 0xFFFFFFFFFFFFFFFF))
+        argv = (ctypes.c_void_p * len(args))(
+            *[ctypes.cast(ctypes.pointer(a), ctypes.c_void_p) for a in args])
+        block = 256
+        grid = (total + block - 1) // block
+        _lib.check(lib.bgx_rtc_launch(handle, grid, block, argv, stream), "bgx_rtc_launch")
+        torch.cuda.synchronize(dev)
+        return keep, hdr, tab
+
+    keep, hdr, tab = launch(-1)
     count = int(hdr[0].item())
     if count:
         first = int(hdr[1].item())
         rows = tab[:min(count, _ERR_SLOTS)].cpu().numpy()
-        rec = next((r for r in rows if int(r[0]) == first), rows[np.argmin(rows[:, 0])])
-        key, kind, _site, dim, index, extent = (int(x) for x in rec)
+        hits = [r for r in rows if int(r[0]) == first]
+        if not hits:
+            # more failing coordinates than record slots and the first one's
+            # record was dropped: re-run that coordinate alone (its own
+            # fresh budget and inputs, as the reference would visit it)
+            _, _, tab1 = launch(first)
+            hits = [tab1[0].cpu().numpy()]
+        key, kind, _site, dim, index, extent = (int(x) for x in hits[0])
         lin = (total - 1 - key) if reverse else key
         tz, r = lin % bz, lin // bz
         ty, r = r % by, r // by

@@ -87,19 +87,37 @@ def ksplit_reduce(partial: torch.Tensor, *, c0: torch.Tensor | None = None, out_
 
 
 _FUSED_CACHE: dict = {}
+FUSED_CACHE_LIMIT = 4   # live FusedKSplit plans (each holds a symmetric-memory buffer)
+
+
+def _fused_plan(key, build):
+    """LRU of FusedKSplit plans keyed by shape/dtype/group.  Ranks call with
+    the same shapes in the same order, so every rank evicts the same plan;
+    an evicted plan releases its symmetric-memory buffer."""
+    f = _FUSED_CACHE.pop(key, None)
+    if f is None:
+        while len(_FUSED_CACHE) >= FUSED_CACHE_LIMIT:
+            _FUSED_CACHE.pop(next(iter(_FUSED_CACHE))).close()
+        f = build()
+    _FUSED_CACHE[key] = f          # most recently used last
+    return f
 
 
 def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
                     c0: torch.Tensor | None = None, out_dtype=None, group=None,
-                    scatter: bool = False, fused: bool = False) -> torch.Tensor:
+                    scatter: bool = False, fused: bool = False,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
     """K-split 2-operand contraction.  ``a_slab``/``b_slab`` hold this rank's
     K range (``k_range``) of the reduction index of ``spec``.  The local
     partial is a tcgen05 (or SIMT) contraction with f32 output; the partials
     are then combined by ``ksplit_reduce`` (one NCCL collective).  Returns the
     full output on every rank, or this rank's row slab with ``scatter``.
     ``fused=True`` (with ``scatter``) runs the GEMM and the reduce-scatter as
-    one kernel (``FusedKSplit``, cached per shape/dtype/group); the returned
-    slab is then ``owned_rows`` of the output (rows per owner rounded to 128)."""
+    one kernel (``FusedKSplit``, cached per shape/dtype/group, at most
+    ``FUSED_CACHE_LIMIT`` live plans); the returned slab is then
+    ``owned_rows`` of the output (rows per owner rounded to 128), copied out
+    of the plan's symmetric buffer into ``out`` (or a fresh tensor), so it
+    stays valid across later calls."""
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
     if fused:
@@ -108,15 +126,16 @@ def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
         key = (spec, tuple(a_slab.shape), tuple(a_slab.stride()), tuple(b_slab.shape),
                tuple(b_slab.stride()), a_slab.dtype, out_dtype, id(group), c0 is not None,
                a_slab.device)
-        f = _FUSED_CACHE.get(key)
-        if f is None:
-            f = _FUSED_CACHE[key] = FusedKSplit(spec, a_slab, b_slab, out_dtype=out_dtype,
-                                                group=group, with_c0=c0 is not None)
+        f = _fused_plan(key, lambda: FusedKSplit(spec, a_slab, b_slab, out_dtype=out_dtype,
+                                                 group=group, with_c0=c0 is not None))
         c0_local = None
         if c0 is not None:
             lo, hi = owned_rows(f.M, f.plan.rows_per_owner, f.rank)
             c0_local = c0[lo:hi]
-        return f(a_slab, b_slab, c0=c0_local)
+        slab = f(a_slab, b_slab, c0=c0_local)
+        if out is None:
+            return slab.clone()
+        return out.copy_(slab)
     partial = contract(spec, a_slab, b_slab, out_dtype=torch.float32)
     return ksplit_reduce(partial, c0=c0, out_dtype=out_dtype or a_slab.dtype, group=group,
                          scatter=scatter)
@@ -204,8 +223,9 @@ class FusedKSplit:
     rows.  Peer buffers come from ``torch.distributed._symmetric_memory``
     (world > 1); one device-side barrier before (slot reuse) and after (all of
     this rank's rows delivered) each call.  ``__call__`` returns this rank's
-    ``owned_rows`` slab (a view of the symmetric buffer: valid until the next
-    call).  This replaces ``ksplit_contract(..., scatter=True)`` (GEMM ->
+    ``owned_rows`` slab as a VIEW of the symmetric buffer: the next call (on
+    this rank, or a peer delivering into it) overwrites it — clone it, or use
+    ``ksplit_contract(fused=True)``, which copies it out.  This replaces ``ksplit_contract(..., scatter=True)`` (GEMM ->
     ``reduce_scatter_tensor`` -> cast) with no NCCL on the data path."""
 
     def __init__(self, spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *, out_dtype=None,
@@ -280,7 +300,14 @@ class FusedKSplit:
         self.c0_buf = (self.buf[offs["c0"]:offs["c0"] + rpo * N * esz].view(self.out_dtype)
                        .view(rpo, N)[:hi - lo]) if with_c0 else None
 
+    def close(self):
+        """Release the symmetric-memory buffer (and local workspaces)."""
+        self.hdl = None
+        self.buf = self.out = self.c0_buf = self.ws = None
+
     def __call__(self, a_slab: torch.Tensor, b_slab: torch.Tensor, c0=None) -> torch.Tensor:
+        if self.buf is None:
+            raise RuntimeError("FusedKSplit used after close()")
         if (c0 is not None) != (self.c0_buf is not None):
             raise ValueError("c0 must be given iff the FusedKSplit was built with_c0=True")
         if c0 is not None:

@@ -133,3 +133,43 @@ def test_compat_installs_run_kernel(dev):
         interp.run_kernel(mod, "vadd", interp.LaunchConfig((2, 1, 1), (4, 1, 1)), bufs)
         assert np.array_equal(bufs[2].data, np.array([11, 22, 33, 44, 55, 66, 77, 88], np.float32))
     assert interp.run_kernel is not fir_gpu.run_kernel
+
+
+def _outcome(fn):
+    try:
+        fn()
+    except interp.InterpError as e:
+        return type(e).__name__, str(e)
+    return None, None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("reverse", [False, True])
+def test_many_failing_threads_report_reference_first(dev, reverse):
+    """more failing coordinates than error-record slots (4792 here
+    vs 1024) must still report the reference's first offending coordinate
+    in its visiting order, with its thread context."""
+    mod = pipeline(VADD_FIR, "vadd", MEM3)
+    launch = interp.LaunchConfig((600, 1, 1), (8, 1, 1))
+    got = _outcome(lambda: fir_gpu.run_kernel(mod, "vadd", launch, vadd_buffers(), reverse=reverse))
+    want = _outcome(lambda: interp.run_kernel(mod, "vadd", launch, vadd_buffers(), reverse=reverse))
+    assert want[0] == "OutOfBounds" and got == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("reverse", [False, True])
+def test_step_budget_vs_out_of_bounds_order(dev, reverse):
+    """Tick-then-execute per op (interp.py:231-233): for every budget, the
+    error kind and message equal the reference's (an OOB access and an
+    overrun inside the same block)."""
+    mod = pipeline(VADD_FIR, "vadd", MEM3)
+    launch = interp.LaunchConfig((3, 1, 1), (4, 1, 1))
+    seen = set()
+    for limit in range(1, 40):
+        got = _outcome(lambda: fir_gpu.run_kernel(mod, "vadd", launch, vadd_buffers(),
+                                                  step_limit=limit, reverse=reverse))
+        want = _outcome(lambda: interp.run_kernel(mod, "vadd", launch, vadd_buffers(),
+                                                  step_limit=limit, reverse=reverse))
+        assert got == want, limit
+        seen.add(want[0])
+    assert seen == {"StepLimitExceeded", "OutOfBounds"}

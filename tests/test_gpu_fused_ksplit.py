@@ -164,6 +164,31 @@ def test_ksplit_contract_fused_flag_single_rank(dev):
         shard.ksplit_contract(MM, a, b, fused=True)
 
 
+def test_ksplit_contract_fused_result_not_aliased(dev):
+    """the returned slab must survive the next call with the same
+    shapes (it used to be a view into the plan's symmetric buffer), caller
+    `out=` is honoured, and the plan cache is bounded (evicted plans release
+    their buffers)."""
+    a = torch.randn(256, 4096, device=dev).bfloat16()
+    b = torch.randn(4096, 256, device=dev).bfloat16()
+    y1 = shard.ksplit_contract(MM, a, b, scatter=True, fused=True)
+    keep = y1.clone()
+    shard.ksplit_contract(MM, 2 * a, b, scatter=True, fused=True)
+    assert torch.equal(y1, keep)
+    out = torch.empty_like(y1)
+    r = shard.ksplit_contract(MM, a, b, scatter=True, fused=True, out=out)
+    assert r is out and torch.equal(out, keep)
+    plans = []
+    for n in range(shard.FUSED_CACHE_LIMIT + 2):
+        bn = torch.randn(4096, 128 + 64 * n, device=dev).bfloat16()
+        shard.ksplit_contract(MM, a, bn, scatter=True, fused=True)
+        plans.append(next(reversed(shard._FUSED_CACHE.values())))
+    assert len(shard._FUSED_CACHE) <= shard.FUSED_CACHE_LIMIT
+    assert plans[0].buf is None            # evicted: buffer released
+    with pytest.raises(RuntimeError, match="after close"):
+        plans[0](a, torch.randn(4096, 128, device=dev).bfloat16())
+
+
 @pytest.mark.parametrize("M,world", [(300, 4), (130, 2), (129, 8), (640, 3)])
 def test_emulated_ragged_owners(dev, M, world):
     """Owners with partial or no rows (rows_per_owner rounded to 128)."""
