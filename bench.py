@@ -5,14 +5,19 @@ Workload (``config.workload``): the sharded 32k-class chain, BASELINE config 5:
     (i,k),(k,j),(j,l)->(i,l)   I = 32768, K = J = L = 8192, bf16 in, f32
     accumulate, bf16 out; executed left to right, (A @ B) @ C
     = 2*I*J*(K+L) = 8,796,093,022,208 flop per step.
-With N GPUs (torchrun) the path partitions along I with no data-path
-collective (B and C replicated), so by default every rank runs its own
-I = 32768-row slab ("scaling": "weak": per-GPU work fixed, job = N slabs);
-``--scaling strong`` instead splits one 32768-row job into N slabs.  value =
-total flop / max over ranks of the device time.
+With N GPUs the path partitions along I with no data-path collective (B and
+C replicated).  ``--gpus N`` launches N ranks itself (torch.distributed.run,
+one process per GPU, 127.0.0.1 rendezvous) unless it already runs under
+torchrun.  The headline is strong scaling ("scaling": "strong"): the fixed
+32768-row job is split into N 128-aligned row slabs (the
+target is >= 7x at 8 GPUs); at N > 1 the weak-scaling figure (every rank its
+own 32768-row slab) is printed alongside under ``weak``.  value = total flop
+/ max over ranks of the device time.
 
 One step = one pass of the hot path over the job with inputs resident in HBM
-(the inputs, A 512 MiB and A@B 512 MiB, exceed the 126 MB L2).  ``e2e`` is the
+(the inputs, A 512 MiB and A@B 512 MiB, exceed the 126 MB L2), made through
+the public API: ``contract(SPEC, A, B, C, out=O)`` — the same call a user
+makes (its planning is memoised; the host gap between launches is reported).  ``e2e`` is the
 same metric through the public host-buffer API (``contract_host``): pinned
 host inputs copied in, result copied out, every step.  ``roofline`` is for
 the dominant kernel (tcgen05 GEMM), timed per launch with CUDA events on its
@@ -223,6 +228,13 @@ def make_inputs(rows, dev, seed):
 
 
 def run_reference(args):
+    """Reference arm: the C port of the reference's loop nest (oracle/, the
+    only other place bench.py executes it) on all host cores.  One step = a
+    bounded sample of the job (16 output elements of row 0 per host thread,
+    each the unfactored K*J-point loop in the reference's order); ``value`` is
+    that sample's throughput, ``ms_per_step`` its measured duration, and the
+    time the whole job would take is reported separately
+    (``job_seconds_extrapolated``)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
@@ -237,19 +249,24 @@ def run_reference(args):
     for _ in range(args.warmup):
         cpu_chain_sample(A0, B, C, n, threads)
     times = [cpu_chain_sample(A0, B, C, n, threads) for _ in range(args.steps)]
-    per_elem = sum(times) / (len(times) * n)
-    total_s = per_elem * I_ * L_
-    value = CHAIN_FLOP / total_s / 1e12
+    step_s = sum(times) / len(times)
+    sample_flop = CHAIN_FLOP * n / (I_ * L_)    # the job's flop share of n outputs
+    value = sample_flop / step_s / 1e12
+    job_s = step_s * (I_ * L_) / n
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_s * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "I": I_, "K": K_, "J": J_, "L": L_,
                    "parallelism": "host cores (OpenMP over outputs)",
-                   "step": f"{n} output elements of the reference loop nest, extrapolated"},
+                   "step": f"{n} output elements of row 0 of the reference loop nest "
+                           f"(a bounded sample of the job)"},
+        "job_seconds_extrapolated": job_s,
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} output elements per step x {args.steps} steps"},
+                         "sample": f"{n} output elements per step x {args.steps} steps "
+                                   f"({step_s:.2f} s per step); the whole job would take "
+                                   f"{job_s:.3e} s"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -437,6 +454,99 @@ def chain_optimal_order(dev):
             "speedup_vs_left_to_right_time": None}
 
 
+def f32_aux(dev):
+    """Like-for-like with the reference's precision (f32 in, f32 out), BASELINE
+    config 4 at 4096^3 through the public ``contract()``: ``mode="exact"``
+    (bit-identical to the reference: fl(fl(a*b) + acc) in increasing k from
+    c0, interp.py:398-416) and ``mode="tf32"`` (tcgen05 kind::tf32, f32
+    accumulate).  The same GEMM's reference arithmetic is timed on a sample
+    of its rows on all host cores (oracle.gemm_kseq, the C port), so
+    ``ratio_exact_vs_cpu_same_config`` compares equal work at equal precision;
+    the sampled rows of the exact result are checked bit-for-bit."""
+    import oracle
+    from paper_2503_04771_b200 import contract
+    n = 4096
+    a_h = np.random.default_rng(1).standard_normal((n, n), dtype=np.float32)
+    b_h = np.random.default_rng(2).standard_normal((n, n), dtype=np.float32)
+    a, b = torch.from_numpy(a_h).to(dev), torch.from_numpy(b_h).to(dev)
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = lambda: flush_buf.zero_()  # noqa: E731
+    res, outs = {}, {}
+    for mode, iters in (("exact", 5), ("tf32", 20)):
+        o = outs[mode] = torch.empty(n, n, device=dev)
+        fn = lambda o=o, mode=mode: contract("(i,k),(k,j)->(i,j)", a, b, out=o, mode=mode)  # noqa: E731
+        for _ in range(2):
+            fn()
+        ms = time_kernel(fn, iters, flush)
+        res[mode] = {"ms": ms, "tflops": 2 * n ** 3 / ms / 1e9}
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    oracle.gemm_kseq(a_h, b_h, rows=(0, threads), threads=threads)
+    per_row = (time.perf_counter() - t0) / threads
+    r = max(threads, min(n, int(6.0 / per_row) // threads * threads))
+    t0 = time.perf_counter()
+    want = oracle.gemm_kseq(a_h, b_h, rows=(0, r), threads=threads)[:r]
+    t_cpu = time.perf_counter() - t0
+    cpu_tf = 2 * r * n * n / t_cpu / 1e12
+    got = outs["exact"][:r].cpu().numpy()
+    res["exact"]["bit_identical_rows_checked"] = r
+    res["exact"]["bit_identical"] = bool(np.array_equal(got, want))
+    res["tf32"]["relF_vs_reference_rows"] = oracle.rel_frobenius(
+        outs["tf32"][:r].cpu().numpy(), want)
+    res["cpu_port_same_config"] = {"tflops": cpu_tf, "cores": threads, "kind": "port",
+                                   "sample": f"rows [0, {r}) of the 4096^3 f32 GEMM, "
+                                             f"{t_cpu:.1f} s"}
+    res["ratio_exact_vs_cpu_same_config"] = res["exact"]["tflops"] / cpu_tf
+    res["ratio_tf32_vs_cpu_same_config"] = res["tf32"]["tflops"] / cpu_tf
+    return res
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(gpus: int) -> int:
+    """``bench.py --gpus N`` outside torchrun: start N ranks (one process per
+    GPU) with torch.distributed.run on a 127.0.0.1 rendezvous, re-running this
+    script with the same arguments; rank 0 prints the JSON line."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dry_run(args, world, rank) -> int:
+    """--dry-run: the multi-rank plumbing without a GPU (gloo): shard the job,
+    barrier, max-over-ranks, one line from rank 0.  Exercised by the CPU tests."""
+    if world > 1:
+        dist.init_process_group("gloo")
+    if args.scaling == "weak":
+        rows, total_rows = I_, I_ * world
+    else:
+        from paper_2503_04771_b200 import shard
+        r0, r1 = shard.row_range(I_, world, rank)
+        rows, total_rows = r1 - r0, I_
+    if world > 1:
+        t = torch.tensor([rows], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        covered = int(t.item())
+    else:
+        covered = rows
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world,
+                          "scaling": args.scaling, "steps": args.steps, "warmup": args.warmup,
+                          "config": {"workload": WORKLOAD, "I": total_rows, "I_per_rank": rows,
+                                     "rows_covered": covered}}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -447,18 +557,25 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-n", type=int, default=0)
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong")
+    ap.add_argument("--dry-run", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
 
     world, rank, local = dist_env()
+    if args.dry_run:
+        return dry_run(args, world, rank)
     # one process per GPU; BGX_DIST_BACKEND=gloo (functional testing of the
     # multi-rank path on fewer GPUs — the data path has no collective, only
     # the barrier / max-over-ranks timing uses the process group)
     backend = os.environ.get("BGX_DIST_BACKEND", "nccl")
+    if backend == "nccl" and world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks but {torch.cuda.device_count()} GPU(s)")
     local_dev = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local_dev)
     dev = torch.device("cuda", local_dev)
@@ -467,51 +584,41 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    from paper_2503_04771_b200 import _lib, executor, shard
+    from paper_2503_04771_b200 import _lib, contract, executor, shard
     from paper_2503_04771_b200.api import contract_host
     _lib.load()
     pk = peaks()
 
-    if args.scaling == "weak":
-        rows, total_rows = I_, I_ * world           # every rank: its own 32768-row slab
-    else:
+    def shard_rows(scaling):
+        if scaling == "weak":
+            return I_, I_ * world                # every rank: its own 32768-row slab
         r0, r1 = shard.row_range(I_, world, rank)
-        rows, total_rows = r1 - r0, I_
+        return r1 - r0, I_
+
+    rows, total_rows = shard_rows(args.scaling)
     job_flop = 2 * total_rows * J_ * (K_ + L_)
     A, B, C = make_inputs(rows, dev, rank)
-    T = torch.empty((rows, J_), dtype=torch.bfloat16, device=dev)
     O = torch.empty((rows, L_), dtype=torch.bfloat16, device=dev)
     sched = {"tile_n": args.tile_n} if args.tile_n else None
     stream = torch.cuda.current_stream()
-    gemm_events = []
 
-    def gemm(a, b, out, m, n, k, record):
-        if record:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        executor.contract_raw(a, (0, k, 1), b, (0, n, 1), out, (0, n, 1), batch=1, M=m, N=n,
-                              K=k, mode="tc", schedule=sched)
-        if record:
-            e1.record(stream)
-            gemm_events.append((e0, e1))
-
-    def step(record=False):
-        gemm(A, B, T, rows, J_, K_, record)      # (i,k),(k,j)->(i,j)
-        gemm(T, C, O, rows, L_, J_, record)      # (i,j),(j,l)->(i,l)
+    def step(a, o):
+        # the public API call: (A @ B) @ C, left to right (the M-shardable order)
+        contract(SPEC, a, B, C, out=o, schedule=sched)
 
     for _ in range(args.warmup):
-        step()
+        step(A, O)
     barrier_sync(world)
     executor.reset_launch_log()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     nsm = _lib.load().bgx_sm_count()
     clk_buf = torch.zeros(2, nsm * 3, dtype=torch.int64, device=dev)
-    with ClockSampler(local_dev) as clk:
+    with ClockSampler(local_dev) as clk, executor.timed_launches() as kev:
         _lib.check(_lib.load().bgx_clock_sample(clk_buf[0].data_ptr(), stream.cuda_stream),
                    "bgx_clock_sample")
         t0.record(stream)
         for _ in range(args.steps):
-            step(record=True)
+            step(A, O)
         t1.record(stream)
         _lib.check(_lib.load().bgx_clock_sample(clk_buf[1].data_ptr(), stream.cuda_stream),
                    "bgx_clock_sample")
@@ -523,7 +630,9 @@ def main():
     ms_local = t0.elapsed_time(t1) / args.steps
     ms = max_over_ranks(ms_local, world)
     value = job_flop / (ms * 1e-3) / 1e12
-    gemm_ms = statistics.mean(a.elapsed_time(b) for a, b in gemm_events)
+    gemm_times = [a.elapsed_time(b) for name, a, b in kev if name.startswith("tcgen05")]
+    kernel_ms_per_step = sum(a.elapsed_time(b) for _, a, b in kev) / args.steps
+    gemm_ms = statistics.mean(gemm_times)
     gemm_flop = 2 * rows * K_ * J_           # both launches are rows x 8192 x 8192
     achieved = gemm_flop / (gemm_ms * 1e-3) / 1e12
 
@@ -579,6 +688,32 @@ def main():
                "d2h_bytes_per_step": total_rows * L_ * 2,
                "api": "paper_2503_04771_b200.api.contract_host (pinned host buffers)",
                "pinned_h2d_GBps_probe": h2d_gbps}
+        del hA, hB, hC, hO
+
+    # weak scaling alongside the strong headline (N > 1): every rank its own
+    # 32768-row slab, same step, same timing rules
+    weak = None
+    if world > 1 and args.scaling == "strong":
+        del O
+        wrows, wtotal = shard_rows("weak")
+        Aw = A if wrows == rows else make_inputs(wrows, dev, rank)[0]
+        del A
+        Ow = torch.empty((wrows, L_), dtype=torch.bfloat16, device=dev)
+        for _ in range(args.warmup):
+            step(Aw, Ow)
+        barrier_sync(world)
+        w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for _ in range(args.steps):
+            step(Aw, Ow)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        wms = max_over_ranks(w0.elapsed_time(w1) / args.steps, world)
+        wflop = 2 * wtotal * J_ * (K_ + L_)
+        weak = {"value": wflop / (wms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": wms,
+                "I": wtotal, "I_per_rank": wrows, "flop_per_step": wflop}
+        del Aw, Ow
+        torch.cuda.empty_cache()
 
     aux = None
     cpu = None
@@ -609,12 +744,16 @@ def main():
     if rank == 0 and world == 1:
         if not args.no_aux:
             aux.update(aux_configs(dev, pk))
+            try:
+                aux["c4_f32_like_for_like"] = f32_aux(dev)
+            except Exception as e:  # noqa: BLE001
+                aux["c4_f32_like_for_like"] = {"error": f"{type(e).__name__}: {e}"[:300]}
             opt = chain_optimal_order(dev)
             opt["speedup_vs_left_to_right_time"] = ms / opt["ms"]
             aux["c5_chain_min_flop_order"] = opt
         if not args.no_cpu:
-            cpu = cpu_baseline(A[:1].float().cpu().numpy(), B.float().cpu().numpy(),
-                               C.float().cpu().numpy())
+            Bh, Ch = B.float().cpu().numpy(), C.float().cpu().numpy()
+            cpu = cpu_baseline(A[:1].float().cpu().numpy(), Bh, Ch)
     # the tile shape the library picked for the chain GEMMs (transparency)
     tile_info = None
     try:
@@ -625,7 +764,7 @@ def main():
         d.o_stride[:] = [0, J_, 1]
         d.in_dtype = d.out_dtype = _lib.BF16
         d.mode = _lib.MODE_TC
-        d.a, d.b, d.out = A.data_ptr(), B.data_ptr(), T.data_ptr()
+        d.a, d.b, d.out = B.data_ptr(), B.data_ptr(), C.data_ptr()
         cg, bn = _lib._i32(), _lib._i32()
         sp, ws = _lib._i32(), _lib._i64()
         _lib.load().bgx_contract_tile(d, cg, bn)
@@ -649,6 +788,7 @@ def main():
                        "J": J_, "L": L_, "parallelism": f"M-shard x{world}",
                        "order": "left-to-right (A@B)@C", "flop_per_step": job_flop,
                        "flop_min_order": CHAIN_FLOP_MINORDER,
+                       "api": "paper_2503_04771_b200.contract(SPEC, A, B, C, out=O)",
                        "l2": "inputs exceed L2 (A 512 MiB, A@B 512 MiB per 1-GPU step)"},
             "fraction_of_peak": value / (pk["bf16"] * world),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"],
@@ -659,8 +799,13 @@ def main():
                          "peak_source": pk["source"] + " burst bf16",
                          "frac_of_sustained": achieved / pk["bf16_sustained"],
                          "frac_of_datasheet_2250": achieved / 2250.0},
+            "host_gap": {"kernel_ms_per_step": kernel_ms_per_step, "step_ms_rank0": ms_local,
+                         "gap_frac": max(0.0, 1 - kernel_ms_per_step / ms_local),
+                         "note": "device time between library launches inside contract() "
+                                 "(planning, allocation, Python) as a fraction of the step"},
             "parity": {"relF_row_samples_max_over_ranks": relF, "tolerance": 1e-2,
                        "oracle": "float64 (A@B)@C on the bf16 inputs"},
+            "weak": weak,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clocks, "aux": aux,
         }
