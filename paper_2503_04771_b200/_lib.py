@@ -13,7 +13,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbgx.so")
+# BGX_LIB: an alternative build of the same library (A/B experiments with
+# csrc/Makefile's `exp` target); the product default is the in-tree .so
+LIB_PATH = os.environ.get("BGX_LIB") or os.path.join(_HERE, "libbgx.so")
 
 MAX_RANK = 8
 MAX_AXES = 12

@@ -116,6 +116,7 @@ int bgx_clock_sample(uint64_t *out, void *stream) {
   cudaGetDevice(&dev);
   constexpr int SMEM = 200 * 1024;   // > half an SM's shared memory: one CTA per SM
   if (!configured[dev & 63]) {
+    RelaxedCaptureScope relaxed;
     BGX_CUDA_TRY(cudaFuncSetAttribute(clock_sample_kernel,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     configured[dev & 63] = 1;

@@ -3,6 +3,9 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
@@ -91,6 +94,30 @@ template <> __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi
 
 // ---------------------------------------------------------------------------
 // PTX wrappers (sm_100a)
+
+// One-time kernel setup (cudaFuncSetAttribute, occupancy queries) may first
+// run while the caller's stream is being captured into a CUDA graph; those
+// calls are not stream work, so switch this thread to relaxed capture mode
+// around them instead of invalidating the caller's capture.
+struct RelaxedCaptureScope {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  RelaxedCaptureScope() { cudaThreadExchangeStreamCaptureMode(&mode); }
+  ~RelaxedCaptureScope() { cudaThreadExchangeStreamCaptureMode(&mode); }
+};
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize = `bytes` for `kern` on the
+// current device, set once per (kernel, device) (capture-safe).
+inline void set_max_smem_once(const void *kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void *, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.insert({kern, dev}).second) {
+    RelaxedCaptureScope relaxed;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -40,6 +40,14 @@
 #ifndef BGX_EPI_DRAIN_BOTH
 #define BGX_EPI_DRAIN_BOTH 1
 #endif
+// 1 (default): staged 32 x 32 output chunks leave shared memory through the
+// LSU — coalesced 16-byte st.global, whole sectors of 8 (16-bit) or 4 (f32)
+// rows per warp instruction — instead of a TMA bulk store, which keeps the
+// SM's TMA unit for operand loads.  B200 A/B (profiles/r02_epilogue_stores.txt):
+// C3 64 x 1024^3 104.4 -> 102.4 us, 4096^3 96.3 -> 95.2 us, chain neutral.
+#ifndef BGX_EPI_LSU
+#define BGX_EPI_LSU 1
+#endif
 
 namespace bgx {
 
@@ -165,6 +173,35 @@ __device__ __forceinline__ void stage_row32(uint8_t *buf, int r, const float *v)
 #pragma unroll
       for (int q = 0; q < 4; ++q) w[q] = pack2<OutT>(v[8 * j + 2 * q], v[8 * j + 2 * q + 1]);
       *reinterpret_cast<uint4 *>(buf + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) = pk;
+    }
+  }
+}
+
+// LSU store of one staged 32 x 32 chunk (the stage_row32 layout): lane l
+// moves 16-byte group l % CPR of row l / CPR (+ RPI rows per step), so each
+// warp instruction writes whole sectors of RPI consecutive rows.
+template <typename OutT>
+__device__ __forceinline__ void lsu_store_chunk(const uint8_t *buf, OutT *row0, int64_t row_stride,
+                                                int64_t rows_valid, int64_t cols_valid, int lane) {
+  constexpr int RB = 32 * (int)sizeof(OutT);   // staged bytes per row (64 or 128)
+  constexpr int CPR = RB / 16;                 // 16-byte groups per row
+  constexpr int RPI = 32 / CPR;                // rows per warp instruction
+  constexpr int EPG = 16 / (int)sizeof(OutT);  // elements per group
+  const int j = lane % CPR;
+#pragma unroll
+  for (int i = 0; i < 32 / RPI; ++i) {
+    const int r = i * RPI + lane / CPR;
+    const int sw = sizeof(OutT) == 4 ? (r & 7) : ((r >> 1) & 3);
+    const uint4 v = *reinterpret_cast<const uint4 *>(buf + r * RB + ((j ^ sw) << 4));
+    if (r < rows_valid) {
+      OutT *dst = row0 + r * row_stride + j * EPG;
+      if ((j + 1) * EPG <= cols_valid) {
+        *reinterpret_cast<uint4 *>(dst) = v;
+      } else {
+        const OutT *e = reinterpret_cast<const OutT *>(&v);
+        for (int q = 0; q < EPG; ++q)
+          if (j * EPG + q < cols_valid) dst[q] = e[q];
+      }
     }
   }
 }
@@ -336,7 +373,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap_a);
     prefetch_tmap(&tmap_b);
-    if (p.tma_store) prefetch_tmap(&tmap_o);
+    if (p.tma_store && !BGX_EPI_LSU) prefetch_tmap(&tmap_o);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CN);   // one commit per pair of the cluster
@@ -739,7 +776,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
               if (n >= p.N) continue;
               uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
               ++chunk;
-              if (lane == 0) bulk_wait_read<1>();
+              if (!BGX_EPI_LSU && lane == 0) bulk_wait_read<1>();
               __syncwarp();
 #pragma unroll
               for (int v4 = 0; v4 < 4; ++v4) {
@@ -747,12 +784,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                                      pk[j][4 * v4 + 3]);
                 *reinterpret_cast<uint4 *>(buf + lane * 64 + ((v4 ^ ((lane >> 1) & 3)) << 4)) = w;
               }
+#if BGX_EPI_LSU
+              __syncwarp();
+              lsu_store_chunk<OutT>(buf, static_cast<OutT *>(p.out) + b * p.so[0] + m_warp * p.so[1] + n,
+                                    p.so[1], p.M - m_warp, p.N - n, lane);
+#else
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
                 tma_store_3d(&tmap_o, buf, (int32_t)n, (int32_t)m_warp, (int32_t)b);
                 bulk_commit();
               }
+#endif
             }
           }
           continue;
@@ -764,15 +807,21 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         if (p.tma_store) {
           uint8_t *buf = ebuf + (chunk & 1) * C::EPI_BUF_BYTES;
           ++chunk;
-          if (lane == 0) bulk_wait_read<1>();   // the buffer used two chunks ago is free
+          if (!BGX_EPI_LSU && lane == 0) bulk_wait_read<1>();   // the buffer used two chunks ago is free
           __syncwarp();
           stage_row32<OutT>(buf, lane, v);
+#if BGX_EPI_LSU
+          __syncwarp();
+          lsu_store_chunk<OutT>(buf, static_cast<OutT *>(p.out) + b * p.so[0] + m_warp * p.so[1] + n,
+                                p.so[1], p.M - m_warp, p.N - n, lane);
+#else
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             tma_store_3d(&tmap_o, buf, (int32_t)n, (int32_t)m_warp, (int32_t)b);
             bulk_commit();
           }
+#endif
         } else if (row_ok) {
           Store<OutT>::row32(orow + n, v, valid >= 32, valid);
         }
@@ -960,7 +1009,9 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   p.tma_store = ((uintptr_t)d.out % 16 == 0) && (d.o_stride[1] * oes) % 16 == 0 &&
                 (d.batch * (p.k_splits > 1 ? p.k_splits : 1) <= 1 ||
                  (d.o_stride[0] * oes) % 16 == 0) && !(p.debug & 2) && !RS;
-  if (p.tma_store) {
+  // (tma_store: the output allows the staged, coalesced epilogue; the map is
+  // only needed when the chunks leave through TMA)
+  if (p.tma_store && !BGX_EPI_LSU) {
     const CUtensorMapDataType odt = oes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                    : (d.out_dtype == BGX_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                                               : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
@@ -993,6 +1044,7 @@ int launch_tc(const bgx_contract_desc &d, const TcParams &p0, cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 63]) {
+    RelaxedCaptureScope relaxed;
     BGX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       C::SMEM_BYTES));
     configured[dev & 63] = 1;
@@ -1049,6 +1101,7 @@ int cn2_slots() {
   int dev = 0;
   cudaGetDevice(&dev);
   if (!cache[dev & 63]) {
+    RelaxedCaptureScope relaxed;
     auto kern = tc_gemm_kernel<BN, 2, OutT, 2, false, 2>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES) !=
         cudaSuccess) {

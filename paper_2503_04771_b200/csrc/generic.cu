@@ -325,7 +325,8 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     if (shared) shared_mask |= 1u << k;
   }
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // once per (kernel, device), at the largest staging this path allows
+    set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
     kern<<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
   };
   if (rows) {
@@ -411,13 +412,21 @@ bool try_chain(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream
     }
   }
   const size_t smem = (size_t)2 * d.n_in * CH_TILE * sizeof(T);
-  if (d.n_in == 1) {
-    cudaFuncSetAttribute(chain_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    chain_kernel<T, 1><<<1, CH_THREADS, smem, s>>>(d, red);
-  } else {
-    cudaFuncSetAttribute(chain_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    chain_kernel<T, 2><<<1, CH_THREADS, smem, s>>>(d, red);
+  static bool configured[2][64] = {{false}};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!configured[d.n_in == 1 ? 0 : 1][dev & 63]) {   // smem is fixed per (T, n_in)
+    RelaxedCaptureScope relaxed;
+    if (d.n_in == 1)
+      cudaFuncSetAttribute(chain_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    else
+      cudaFuncSetAttribute(chain_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured[d.n_in == 1 ? 0 : 1][dev & 63] = true;
   }
+  if (d.n_in == 1)
+    chain_kernel<T, 1><<<1, CH_THREADS, smem, s>>>(d, red);
+  else
+    chain_kernel<T, 2><<<1, CH_THREADS, smem, s>>>(d, red);
   *rc = check_launch("chain_kernel");
   return true;
 }

@@ -17,6 +17,8 @@ re-planning).
 
 from __future__ import annotations
 
+import gc
+
 import torch
 
 from . import _lib, executor
@@ -111,8 +113,19 @@ class Prepared:
         self._launch(self.inputs, self.out, self.c0)   # warm-up: one-time init outside capture
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._launch(self.inputs, self.out, self.c0)
+        # No cyclic garbage collection while capturing: a collection could
+        # finalise an unreachable earlier graph (cudaGraphExecDestroy), which is
+        # illegal during a capture and invalidates it (torch.cuda.graph only
+        # collects once, before the capture starts).  thread_local: other
+        # threads' CUDA calls cannot invalidate this capture either.
+        gc_was_enabled = gc.isenabled()
+        gc.disable()
+        try:
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._launch(self.inputs, self.out, self.c0)
+        finally:
+            if gc_was_enabled:
+                gc.enable()
         self._graph = g
 
     def __call__(self, *tensors: torch.Tensor, out=None, c0=None) -> torch.Tensor:
