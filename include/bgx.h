@@ -256,6 +256,47 @@ BGX_API int bgx_contract_reduce_scatter(const bgx_contract_desc *d, const bgx_re
                                         void *stream);
 BGX_API int bgx_rs_reduce(const bgx_contract_desc *d, const bgx_reduce_scatter *rs, void *stream);
 
+/* ---- one process, several devices: the M-shard -------------
+ * The contraction's output rows (or batches) are split into n independent
+ * slabs; descs[i] describes slab i with pointers on device devices[i] (A's
+ * rows / batches of that slab, B whole, that slab of c0 and out) and
+ * streams[i] is a stream on that device (NULL: its legacy default stream;
+ * `streams` itself may be NULL).  Each slab is launched with bgx_contract on
+ * its own device — launches are asynchronous, so the devices run
+ * concurrently — and the caller's current device is restored.  No data moves
+ * between devices (there is no exchange in the M-shard); slabs are computed
+ * exactly as one device would compute those rows.  Stops at the first
+ * failing slab (bgx_last_error names it). */
+BGX_API int bgx_contract_sharded(const bgx_contract_desc *descs, const int32_t *devices,
+                                 void *const *streams, int32_t n);
+
+/* ---- the K-split exchange over NCCL ------------------------
+ * NCCL is loaded at run time (the copy already in the process, else
+ * libnccl.so.2); BGX_ERR_UNSUPPORTED without it.  One communicator per rank
+ * (one process per GPU, or one thread per GPU), created collectively:
+ *   rank 0: bgx_nccl_unique_id(id) -> share the 128 bytes with every rank ->
+ *   every rank on its device: bgx_nccl_comm_init(&comm, world, rank, id).
+ * bgx_ksplit_reduce(partial, out, c0, out_dtype, rows, cols, scatter, ws,
+ * comm, stream): `partial` is this rank's rows x cols f32 partial sum (its K
+ * slab's contribution, e.g. from bgx_contract with out_dtype f32); the
+ * partials are summed over the ranks with ncclReduceScatter (scatter != 0:
+ * rows % world == 0, this rank receives rows [rank*rows/world, ...) into
+ * `out`) or ncclAllReduce (every rank receives all rows), in f32, then c0
+ * (same rows, out_dtype) is added and the result cast to out_dtype
+ * (bgx_cast_f32).  `ws` is an f32 workspace of the received size, needed
+ * unless out_dtype is f32 and c0 is NULL (then NCCL writes `out` directly).
+ * Stream-ordered; the summation order across ranks is NCCL's. */
+BGX_API int bgx_nccl_unique_id(void *id_out /* 128 bytes */);
+BGX_API int bgx_nccl_comm_init(void **comm, int32_t world, int32_t rank, const void *id);
+BGX_API int bgx_nccl_comm_destroy(void *comm);
+BGX_API int bgx_ksplit_reduce(const float *partial, void *out, const void *c0, int32_t out_dtype,
+                              int64_t rows, int64_t cols, int32_t scatter, float *ws, void *comm,
+                              void *stream);
+/* Releases the library's per-process state (unloads NCCL once every
+ * communicator is destroyed).  The library holds no device memory of its
+ * own: workspaces are always the caller's. */
+BGX_API int bgx_shutdown(void);
+
 /* ---- elementwise helpers for multi-GPU K-split -------------------------
  * out[i] = (dtype_out) src[i] for n elements, src f32 (the reduced partials),
  * out f32/bf16/f16; with c0 != NULL adds c0[i] first (in f32).           */

@@ -110,6 +110,13 @@ SIGNATURES = {
     "bgx_rtc_launch": (ctypes.c_int, [_vp, ctypes.c_uint64, ctypes.c_uint32,
                                       ctypes.POINTER(_vp), _vp]),
     "bgx_rtc_free": (ctypes.c_int, [_vp]),
+    "bgx_contract_sharded": (ctypes.c_int, [ctypes.POINTER(BgxContractDesc), ctypes.POINTER(_i32),
+                                            ctypes.POINTER(_vp), _i32]),
+    "bgx_nccl_unique_id": (ctypes.c_int, [_vp]),
+    "bgx_nccl_comm_init": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _i32, _vp]),
+    "bgx_nccl_comm_destroy": (ctypes.c_int, [_vp]),
+    "bgx_ksplit_reduce": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
+    "bgx_shutdown": (ctypes.c_int, []),
 }
 
 

@@ -56,26 +56,32 @@ def _emit(text: str, out_path):
         sys.stdout.write(text)
 
 
+def _shape_of(part: str) -> tuple:
+    """``"4x8"`` -> ``(4, 8)``; anything else is bridgegen's 'bad shape'."""
+    token = part.strip()
+    dims = token.split("x")
+    if any(not d.isdigit() for d in dims):
+        raise CliError(f"bad shape '{token}'")
+    return tuple(map(int, dims))
+
+
 def check_shapes(spec: E.EinsumSpec, text: str):
-    """Operand shapes from ``AxB,...`` with bridgegen's checks and messages
-    (cli.py:302-322)."""
-    shapes = []
-    for part in text.split(","):
-        dims = part.strip().split("x")
-        if not all(d.isdigit() for d in dims):
-            raise CliError(f"bad shape '{part.strip()}'")
-        shapes.append(tuple(int(d) for d in dims))
-    tuples = spec.inputs + (spec.output,)
-    if len(shapes) != len(tuples):
-        raise CliError(f"{len(tuples)} operand shape(s) expected, got {len(shapes)}")
-    extent = {}
-    for shape, tup in zip(shapes, tuples):
+    """Operand shapes from ``AxB,...`` (inputs, then the output), validated
+    against the spec with the messages bridgegen's ``einsum`` subcommand
+    prints (cli.py:302-322): shape syntax, operand count, rank per operand,
+    one extent per index."""
+    shapes = [_shape_of(part) for part in text.split(",")]
+    operands = (*spec.inputs, spec.output)
+    if len(shapes) != len(operands):
+        raise CliError(f"{len(operands)} operand shape(s) expected, got {len(shapes)}")
+    bound: dict = {}
+    for shape, tup in zip(shapes, operands):
         if len(shape) != len(tup):
             raise CliError(f"shape {shape} does not match index tuple {tup}")
-        for d, name in zip(shape, tup):
-            if name in extent and extent[name] != d:
-                raise CliError(f"index '{name}' has inconsistent extents {extent[name]} and {d}")
-            extent[name] = d
+        for name, d in zip(tup, shape):
+            first = bound.setdefault(name, d)
+            if first != d:
+                raise CliError(f"index '{name}' has inconsistent extents {first} and {d}")
     return shapes
 
 

@@ -430,13 +430,11 @@ def _exec_cache() -> dict:
     return _trace.exec_cache
 
 
-def _fast_gemm(plan, spec, inputs, c0, out, mode, log: bool = True):
-    """Pre-built descriptor for a plain GEMM (no operand copy, no output
-    permute, no split-K workspace, no padding): later calls with the same
-    signature patch the pointers and call bgx_contract directly — what
-    ``prepare()`` does (it builds its GEMM launcher here too), applied
-    automatically to repeated ``execute`` calls (the reference-shaped
-    ``run_function`` path of BASELINE config 1)."""
+def gemm_descriptor(plan, spec, inputs, c0, out, mode):
+    """A complete ``bgx_contract_desc`` for a plain GEMM plan — no operand
+    copy, no output permute, no split-K workspace, no padding — or None when
+    the plan needs any of those (the planner's full path handles it).
+    Returns ``(desc, kind)``."""
     if plan.a_view.needs_copy or plan.b_view.needs_copy or mode == "tf32":
         return None
     ext = extents_of(spec, [t.shape for t in inputs] + [out.shape])
@@ -457,15 +455,31 @@ def _fast_gemm(plan, spec, inputs, c0, out, mode, log: bool = True):
     d.mode = MODES[mode]
     d.a, d.b, d.out = inputs[ia].data_ptr(), inputs[ib].data_ptr(), out.data_ptr()
     d.c0 = c0.data_ptr() if c0 is not None else None
-    kind = lib.bgx_contract_kernel(d)
-    if kind < 0 or (kind == _lib.KERNEL_SIMT16 and mode == "auto"
-                    and 2 * plan.batch * plan.M * plan.N * plan.K >= PAD_MIN_FLOP):
-        return None
-    if kind == _lib.KERNEL_TC:
-        sp, ws = _lib._i32(1), _lib._i64(0)
-        _lib.check(lib.bgx_contract_splitk_plan(d, sp, ws), "bgx_contract_splitk_plan")
-        if sp.value != 1:
+    with _on_device(out.device):
+        kind = lib.bgx_contract_kernel(d)
+        if kind < 0 or (kind == _lib.KERNEL_SIMT16 and mode == "auto"
+                        and 2 * plan.batch * plan.M * plan.N * plan.K >= PAD_MIN_FLOP):
             return None
+        if kind == _lib.KERNEL_TC:
+            sp, ws = _lib._i32(1), _lib._i64(0)
+            _lib.check(lib.bgx_contract_splitk_plan(d, sp, ws), "bgx_contract_splitk_plan")
+            if sp.value != 1:
+                return None
+    return d, kind
+
+
+def _fast_gemm(plan, spec, inputs, c0, out, mode, log: bool = True):
+    """Pre-built descriptor for a plain GEMM (``gemm_descriptor``): later
+    calls with the same signature patch the pointers and call bgx_contract
+    directly — what ``prepare()`` does (it builds its GEMM launcher here too),
+    applied automatically to repeated ``execute`` calls (the reference-shaped
+    ``run_function`` path of BASELINE config 1)."""
+    got = gemm_descriptor(plan, spec, inputs, c0, out, mode)
+    if got is None:
+        return None
+    d, kind = got
+    ia, ib = plan.a, plan.b
+    lib = _lib.load()
     name = _lib.KERNEL_NAMES.get(kind, "contract")
 
     def run(xs, o, c):

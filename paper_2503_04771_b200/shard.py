@@ -19,6 +19,8 @@ for the plumbing.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -43,11 +45,33 @@ def k_range(total: int, world: int, rank: int, align: int = 64):
     return row_range(total, world, rank, align)
 
 
-def sharded_contract(spec, *local_operands, **kw) -> torch.Tensor:
-    """M-sharded contraction: every rank passes its own slab of the first
-    operand (rows ``row_range``) and the full remaining operands; returns the
-    rank's output slab.  No communication."""
-    return contract(spec, *local_operands, **kw)
+def sharded_contract(spec, *operands, group=None, align: int = 128, **kw):
+    """M-sharded contraction, one process per GPU: every rank passes the FULL
+    (replicated) operands; this rank contracts only its output row slab —
+    rows ``row_range`` of the output's leading index, from the operand views
+    ``shard_operands`` cuts (narrowed along that index, the rest whole) — and
+    returns ``(lo, hi, slab)``.  No communication: the slabs are independent
+    and each is computed exactly as on one device (§8e).  ``group`` (default:
+    the world group when torch.distributed is initialised, else a single
+    rank) gives world size and rank."""
+    if not isinstance(spec, EinsumSpec):
+        spec = parse_einsum(spec)
+    if not spec.output:
+        raise ValueError(f"{spec}: a rank-0 output has no rows to shard")
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    else:
+        world, rank = 1, 0
+    lo, hi, views = shard_operands(spec, operands, world, rank, align)
+    if hi <= lo:   # more ranks than row slabs: this rank owns nothing
+        from .api import output_shape
+        shape = output_shape(spec, operands)
+        dt = kw.get("out_dtype") or operands[0].dtype
+        return lo, hi, torch.empty((0, *shape[1:]), dtype=dt, device=operands[0].device)
+    c0 = kw.pop("c0", None)
+    if c0 is not None:
+        c0 = c0[lo:hi]
+    return lo, hi, contract(spec, *views, c0=c0, **kw)
 
 
 def _cast(src: torch.Tensor, out: torch.Tensor, c0: torch.Tensor | None):
@@ -60,13 +84,80 @@ def _cast(src: torch.Tensor, out: torch.Tensor, c0: torch.Tensor | None):
     return out
 
 
+class NcclComm:
+    """The library's own NCCL communicator (C ABI ``bgx_nccl_*``), for the
+    native K-split exchange ``bgx_ksplit_reduce``.  Created collectively: rank
+    0 draws the unique id and the process group (``group``, default world)
+    broadcasts it; every rank initialises on its current device.  Without a
+    process group it is a single-rank communicator."""
+
+    def __init__(self, group=None):
+        lib = _lib.load()
+        if dist.is_available() and dist.is_initialized():
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(lib.bgx_nccl_unique_id(uid), "bgx_nccl_unique_id")
+        if self.world > 1:
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0)
+                                       if group is not None else 0, group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        handle = _lib._vp()
+        _lib.check(lib.bgx_nccl_comm_init(ctypes.byref(handle), self.world, self.rank, uid),
+                   "bgx_nccl_comm_init")
+        self.handle = handle
+
+    def close(self):
+        if self.handle is not None and self.handle.value:
+            _lib.check(_lib.load().bgx_nccl_comm_destroy(self.handle), "bgx_nccl_comm_destroy")
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+
+
+def _ksplit_reduce_native(partial, comm: NcclComm, c0, dt, scatter):
+    """bgx_ksplit_reduce: ncclReduceScatter / ncclAllReduce of the f32
+    partials inside libbgx, then c0 + cast (bgx_cast_f32)."""
+    rows = partial.shape[0]
+    cols = partial.numel() // max(1, rows)
+    scatter = bool(scatter and rows % comm.world == 0)
+    got = rows // comm.world if scatter else rows
+    out = torch.empty((got, *partial.shape[1:]), dtype=dt, device=partial.device)
+    c0_local = (c0[comm.rank * got:(comm.rank + 1) * got] if scatter else c0) \
+        if c0 is not None else None
+    ws = None
+    if not (dt == torch.float32 and c0_local is None):
+        ws = torch.empty(out.shape, dtype=torch.float32, device=partial.device)
+    _lib.check(_lib.load().bgx_ksplit_reduce(
+        partial.contiguous().data_ptr(), out.data_ptr(),
+        c0_local.contiguous().data_ptr() if c0_local is not None else None,
+        executor.TORCH_TO_BGX[dt], rows, cols, 1 if scatter else 0,
+        ws.data_ptr() if ws is not None else None, comm.handle,
+        torch.cuda.current_stream(partial.device).cuda_stream), "bgx_ksplit_reduce")
+    executor._log("ksplit-reduce")
+    return out
+
+
 def ksplit_reduce(partial: torch.Tensor, *, c0: torch.Tensor | None = None, out_dtype=None,
-                  group=None, scatter: bool = False, cast=None) -> torch.Tensor:
+                  group=None, scatter: bool = False, cast=None,
+                  comm: NcclComm | None = None) -> torch.Tensor:
     """Reduce this rank's f32 partial sums of a K-split contraction over the
     process group — ``reduce_scatter_tensor`` (each rank keeps its row slab)
     when ``scatter`` and the rows divide evenly, else ``all_reduce`` — then
-    add ``c0`` and cast to ``out_dtype`` with ``bgx_cast_f32``.  ``cast`` is
-    injectable only so the collective logic can be tested on CPU with gloo."""
+    add ``c0`` and cast to ``out_dtype`` with ``bgx_cast_f32``.  With
+    ``comm`` (an ``NcclComm``) the whole exchange runs inside libbgx
+    (``bgx_ksplit_reduce``: the library's own NCCL communicator) instead of
+    through torch.distributed.  ``cast`` is injectable only so the collective
+    logic can be tested on CPU with gloo."""
+    if comm is not None:
+        return _ksplit_reduce_native(partial, comm, c0, out_dtype or partial.dtype, scatter)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     dt = out_dtype or partial.dtype
     if world > 1 and scatter and partial.shape[0] % world == 0:
@@ -106,7 +197,8 @@ def _fused_plan(key, build):
 def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
                     c0: torch.Tensor | None = None, out_dtype=None, group=None,
                     scatter: bool = False, fused: bool = False,
-                    out: torch.Tensor | None = None) -> torch.Tensor:
+                    out: torch.Tensor | None = None,
+                    comm: NcclComm | None = None) -> torch.Tensor:
     """K-split 2-operand contraction.  ``a_slab``/``b_slab`` hold this rank's
     K range (``k_range``) of the reduction index of ``spec``.  The local
     partial is a tcgen05 (or SIMT) contraction with f32 output; the partials
@@ -117,7 +209,8 @@ def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
     ``FUSED_CACHE_LIMIT`` live plans); the returned slab is then
     ``owned_rows`` of the output (rows per owner rounded to 128), copied out
     of the plan's symmetric buffer into ``out`` (or a fresh tensor), so it
-    stays valid across later calls."""
+    stays valid across later calls.  ``comm``: exchange through libbgx's own
+    NCCL communicator (``bgx_ksplit_reduce``) instead of torch.distributed."""
     if not isinstance(spec, EinsumSpec):
         spec = parse_einsum(spec)
     if fused:
@@ -138,7 +231,7 @@ def ksplit_contract(spec, a_slab: torch.Tensor, b_slab: torch.Tensor, *,
         return out.copy_(slab)
     partial = contract(spec, a_slab, b_slab, out_dtype=torch.float32)
     return ksplit_reduce(partial, c0=c0, out_dtype=out_dtype or a_slab.dtype, group=group,
-                         scatter=scatter)
+                         scatter=scatter, comm=comm)
 
 
 # ---------------------------------------------------------------------------
@@ -426,7 +519,9 @@ def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> 
     ``devices[r]`` (peer copies over NVLink), each device contracts its slab
     on its own current stream — launches are asynchronous, so the devices run
     concurrently — and the slabs are copied back into ``out`` on the
-    operands' device.  Covers contractions (leading index from operand 0, 1,
+    operands' device.  When every slab is a plain GEMM the slabs are launched
+    by ONE C-ABI call, ``bgx_contract_sharded`` (a descriptor per slab, each
+    on its own device and stream).  Covers contractions (leading index from operand 0, 1,
     or several operands) and permutations (a transpose's output rows are a
     strided column slab of its input, §8e).  No collective: the slabs are
     independent, so every row is computed as on one device — bit for bit
@@ -446,7 +541,8 @@ def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> 
     c0 = kw.pop("c0", None)
     rows = shape[0]
     n = len(devices)
-    pending = []
+    # stage every slab on its device (peer copies), then launch
+    slabs = []
     for r, dev in enumerate(devices):
         lo, hi = row_range(rows, n, r)
         if hi <= lo:
@@ -454,8 +550,28 @@ def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> 
         with torch.cuda.device(dev):
             local = [t.to(dev, non_blocking=True) for t in lead_slabs(spec, operands, lo, hi)]
             cc = c0[lo:hi].to(dev, non_blocking=True) if c0 is not None else None
-            y = contract(spec, *local, c0=cc, **kw)
-            done = torch.cuda.Event()
+            y = torch.empty((hi - lo, *shape[1:]), dtype=dt, device=dev)
+        slabs.append((lo, hi, dev, local, cc, y))
+    descs = _sharded_descriptors(spec, slabs, kw) if slabs else None
+    if descs is not None:
+        # every slab is a plain GEMM: ONE C-ABI call launches them all, each
+        # on its own device and current stream (bgx_contract_sharded)
+        lib = _lib.load()
+        arr = (_lib.BgxContractDesc * len(descs))(*descs)
+        devs = (_lib._i32 * len(descs))(*[dev.index for _, _, dev, *_ in slabs])
+        streams = (_lib._vp * len(descs))(*[torch.cuda.current_stream(dev).cuda_stream
+                                              for _, _, dev, *_ in slabs])
+        _lib.check(lib.bgx_contract_sharded(arr, devs, streams, len(descs)),
+                   "bgx_contract_sharded")
+        executor._log("sharded")
+    else:
+        for lo, hi, dev, local, cc, y in slabs:
+            with torch.cuda.device(dev):
+                contract(spec, *local, c0=cc, out=y, **kw)
+    pending = []
+    for lo, hi, dev, local, cc, y in slabs:
+        done = torch.cuda.Event()
+        with torch.cuda.device(dev):
             done.record(torch.cuda.current_stream(dev))
         pending.append((lo, hi, y, done))
     home_stream = torch.cuda.current_stream(home)
@@ -463,3 +579,25 @@ def contract_devices(spec, *operands: torch.Tensor, devices, out=None, **kw) -> 
         home_stream.wait_event(done)
         out[lo:hi].copy_(y, non_blocking=True)
     return out
+
+
+def _sharded_descriptors(spec, slabs, kw):
+    """One bgx_contract_desc per slab when every slab is a plain GEMM the
+    planner would launch as one bgx_contract (executor.gemm_descriptor), else
+    None (permutations, chains, operand copies, split-K: per-device path)."""
+    if kw.get("schedule") or kw.get("chain_order", "left") != "left" or len(spec.inputs) != 2:
+        return None
+    mode = kw.get("mode", "auto")
+    from .plan import GemmPlan
+    descs = []
+    for lo, hi, dev, local, cc, y in slabs:
+        if any(t.dtype != local[0].dtype for t in local):
+            return None
+        plan = executor.plan_for(spec, local, y, mode=mode)
+        if not isinstance(plan, GemmPlan):
+            return None
+        got = executor.gemm_descriptor(plan, spec, local, cc, y, mode)
+        if got is None:
+            return None
+        descs.append(got[0])
+    return descs

@@ -38,6 +38,8 @@ def run(shape, variants):
         for k, v in kw.items():
             if k == "debug":
                 d.sched.reserved[0] = v
+            elif k == "pf":
+                d.sched.reserved[2] = v
             elif k == "cluster_n":
                 d.sched.reserved[1] = v
             else:
@@ -61,6 +63,8 @@ def run(shape, variants):
 
 
 VARS = {
+    "pf": [("auto", {}), ("auto pf4", {"pf": 4}), ("auto pf8", {"pf": 8}),
+           ("auto pf16", {"pf": 16}), ("auto pf32", {"pf": 32}), ("auto again", {})],
     "cn2f": [("t256 quads dyn", {"tile_n": 256, "cta_group": 2, "cluster_n": 2, "debug": 128}),
              ("t256 quads queue-static", {"tile_n": 256, "cta_group": 2, "cluster_n": 2, "debug": 128 + 2048}),
              ("t256 quads static", {"tile_n": 256, "cta_group": 2, "cluster_n": 2, "debug": 128 + 512})],

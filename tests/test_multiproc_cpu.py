@@ -112,8 +112,8 @@ _SHARD_SPECS = [("(i,k),(k,j)->(i,j)", [(300, 40), (40, 24)]),
 
 def _torch_einsum(spec, ops):
     """CPU stand-in for the per-rank contraction (bracket spec -> torch.einsum)."""
-    from paper_2503_04771_b200.einsum import parse_einsum
-    sp = parse_einsum(spec)
+    from paper_2503_04771_b200.einsum import EinsumSpec, parse_einsum
+    sp = spec if isinstance(spec, EinsumSpec) else parse_einsum(spec)
     letters = {ax: chr(97 + n) for n, ax in enumerate(sp.axes)}
     eq = ",".join("".join(letters[a] for a in t) for t in sp.inputs)
     return torch.einsum(eq + "->" + "".join(letters[a] for a in sp.output), *ops)
@@ -164,3 +164,47 @@ def test_lead_slabs_views():
     assert sa.shape == (40, 64) and sa.data_ptr() == a[:, 100:].data_ptr() and sb is b
     with pytest.raises(ValueError, match="rank-0"):
         shard.lead_slabs("(i),(i)->()", [a[0], a[1]], 0, 1)
+
+
+def _sharded_contract_worker(rank, world, port, q):
+    """shard.sharded_contract's host logic (rank/world from the process group,
+    the slab views, the c0 slab) with the per-rank contraction stood in by
+    torch.einsum on CPU (the CUDA path is tests/test_gpu_sharded.py)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def fake_contract(spec, *ops, c0=None, **kw):
+            out = _torch_einsum(spec, ops)
+            return out if c0 is None else out + c0
+        shard.contract = fake_contract
+        oks = []
+        for n, (spec, shapes) in enumerate(_SHARD_SPECS):
+            g = torch.Generator().manual_seed(n)
+            ops = [torch.randn(s, generator=g, dtype=torch.float64) for s in shapes]
+            full = _torch_einsum(spec, ops)
+            c0 = torch.randn(full.shape, generator=g, dtype=torch.float64)
+            lo, hi, mine = shard.sharded_contract(spec, *ops, c0=c0, align=16)
+            parts = [None] * world
+            dist.all_gather_object(parts, (lo, hi, mine))
+            stitched = torch.cat([p[2] for p in sorted(parts, key=lambda t: t[0])])
+            oks.append(torch.allclose(stitched, full + c0, rtol=1e-12, atol=1e-12))
+        q.put((rank, *oks))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_contract_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_contract_worker, args=(r, world, port, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for rank, *oks in sorted(q.get() for _ in range(world)):
+        assert all(oks), (rank, oks)
