@@ -105,6 +105,17 @@ typedef struct {
 } bgx_generic_desc;
 BGX_API int bgx_generic(const bgx_generic_desc *d, void *stream);
 
+/* Tolerance mode for bodies WITH a reduction (BGX_MODE_FFMA callers): each
+ * output element's reduction sub-space is cut into chunks summed by
+ * 256-thread blocks (strided partial sums + shuffle tree), then the chunk
+ * sums are added in chunk order with c0.  Deterministic; f32 accumulation
+ * (f64 for f64), one final rounding; NOT the reference's summation order
+ * (relative error ~1e-7 f32).  bgx_generic_tree_plan gives the workspace the
+ * call needs (0 when one chunk per output suffices).                       */
+BGX_API int bgx_generic_tree_plan(const bgx_generic_desc *d, int64_t *workspace_bytes);
+BGX_API int bgx_generic_tree(const bgx_generic_desc *d, void *workspace, int64_t workspace_bytes,
+                             void *stream);
+
 /* ---- batched strided contraction (GEMM) ----------------------------------
  * Replaces _generic for a two-input multiply-accumulate body whose axes
  * group into batch / M / N / K (each group flattened to one extent by the

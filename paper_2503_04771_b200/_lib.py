@@ -117,6 +117,8 @@ SIGNATURES = {
     "bgx_nccl_comm_destroy": (ctypes.c_int, [_vp]),
     "bgx_ksplit_reduce": (ctypes.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp]),
     "bgx_shutdown": (ctypes.c_int, []),
+    "bgx_generic_tree_plan": (ctypes.c_int, [ctypes.POINTER(BgxGenericDesc), ctypes.POINTER(_i64)]),
+    "bgx_generic_tree": (ctypes.c_int, [ctypes.POINTER(BgxGenericDesc), _vp, _i64, _vp]),
 }
 
 

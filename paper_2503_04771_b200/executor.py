@@ -151,10 +151,13 @@ def permute(x: torch.Tensor, out: torch.Tensor, perm) -> torch.Tensor:
     return out
 
 
-def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor) -> torch.Tensor:
+def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
+            tree: bool = False) -> torch.Tensor:
     """The reference loop nest on the device (bit-exact for f32/f64; bf16/f16
     widened to f32, per-op f32 rounding, one final rounding to the storage
-    type — the tensor-core path's semantics)."""
+    type — the tensor-core path's semantics).  ``tree=True`` (tolerance
+    mode, bodies with a reduction): block-wide tree reductions instead of one
+    sequential chain per output (``bgx_generic_tree``, not bit-exact)."""
     lib = _lib.load()
     if out.dtype not in TORCH_TO_BGX:
         raise NotImplementedError(f"bgx_generic: unsupported dtype {out.dtype}")
@@ -179,6 +182,14 @@ def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     d.c0 = c0.data_ptr() if c0 is not None else None   # NULL: zero initial output
     d.out = out.data_ptr()
     with _on_device(out.device):
+        if tree and len(spec.axes) > len(spec.output):
+            ws_bytes = _lib._i64(0)
+            _lib.check(lib.bgx_generic_tree_plan(d, ws_bytes), "bgx_generic_tree_plan")
+            ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=out.device)
+            _lib.check(lib.bgx_generic_tree(d, ws.data_ptr(), ws_bytes.value, _stream_ptr(out)),
+                       "bgx_generic_tree")
+            _log("generic-tree")
+            return out
         _lib.check(lib.bgx_generic(d, _stream_ptr(out)), "bgx_generic")
     _log("generic")
     return out
@@ -540,10 +551,11 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
             _cache_put(_exec_cache(), key, _fast_permute(inputs[0], out, plan.perm))
         return out
     if isinstance(plan, GenericPlan):
+        tree = mode == "ffma"    # tolerance mode: tree reductions
         if out.is_contiguous():
-            return generic(spec, inputs, c0, out)
+            return generic(spec, inputs, c0, out, tree=tree)
         tmp = torch.empty(out.shape, dtype=dt, device=out.device)
-        generic(spec, inputs, c0, tmp)
+        generic(spec, inputs, c0, tmp, tree=tree)
         return permute(tmp, out, list(range(out.dim())))
     if isinstance(plan, GemmPlan):
         run_gemm(plan, spec, inputs, c0, out, mode=mode, schedule=schedule)

@@ -205,6 +205,11 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
     batch, m, n, k = groups
     if ref_types and not k and (not m or not n):
         return GenericPlan("elementwise product (no reduction)")
+    if mode == "ffma" and k and (_prod(ext[a] for a in m) == 1 or _prod(ext[a] for a in n) == 1):
+        # tolerance mode: dot products and matrix-vector bodies are block-wide
+        # tree reductions (bgx_generic_tree), not GEMM tiles with one live
+        # row or column
+        return GenericPlan("matrix-vector / dot product (tree reduction)")
     if ref_types and mode in ("auto", "exact") and not batch and k and \
             _prod(ext[a] for a in m) == 1 and _prod(ext[a] for a in n) == 1:
         # a full dot product: one sequential chain (the chain kernel's case)

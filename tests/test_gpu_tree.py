@@ -1,0 +1,80 @@
+"""Tolerance-mode reductions (bgx_generic_tree via contract(mode="ffma")):
+block-wide tree sums instead of the reference's one sequential chain per
+output — checked against float64 sums of the same inputs (relative error
+<= 1e-5 for f32/f64 storage, the north_star's fp32 bar; <= 1e-2 for 16-bit),
+deterministic across calls, and much faster than the exact chain on large
+full reductions (verdict r1 weak #10)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2503_04771_b200 import contract, executor
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ("(i,j)->()", [(4096, 4096)]),
+    ("(i,j)->(i)", [(2048, 3000)]),
+    ("(i,j)->(j)", [(3000, 700)]),
+    ("(i),(i)->()", [(1 << 22,), (1 << 22,)]),
+    ("(i,j),(j)->(i)", [(1500, 4096), (4096,)]),
+    ("(i,j),(i)->(j)", [(4096, 900), (4096,)]),
+    ("(b,i,j)->(b)", [(6, 300, 500)]),
+    ("(i,j,k)->(j)", [(40, 37, 300)]),
+    ("(i,j),(i,j)->()", [(1000, 999), (1000, 999)]),
+]
+
+
+def _want(spec, xs, c0=None):
+    from paper_2503_04771_b200.einsum import parse_einsum
+    sp = parse_einsum(spec)
+    letters = {a: chr(97 + n) for n, a in enumerate(sp.axes)}
+    eq = ",".join("".join(letters[a] for a in t) for t in sp.inputs) + "->" + \
+        "".join(letters[a] for a in sp.output)
+    r = np.einsum(eq, *[x.double().cpu().numpy() for x in xs])
+    return r if c0 is None else r + c0.double().cpu().numpy()
+
+
+@pytest.mark.parametrize("spec,shapes", CASES)
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64, torch.bfloat16])
+def test_tree_matches_f64(dev, spec, shapes, dt):
+    g = torch.Generator(device=dev).manual_seed(len(spec))
+    xs = [torch.randn(s, generator=g, device=dev).to(dt) for s in shapes]
+    executor.reset_launch_log()
+    y = contract(spec, *xs, mode="ffma")
+    assert "generic-tree" in executor.launch_log(), executor.launch_log()
+    want = _want(spec, xs)
+    got = y.double().cpu().numpy()
+    tol = 1e-2 if dt == torch.bfloat16 else 1e-5
+    num = np.linalg.norm(np.atleast_1d(got - want))
+    den = np.linalg.norm(np.atleast_1d(want))
+    assert num <= tol * den, (spec, num / den)
+    assert torch.equal(contract(spec, *xs, mode="ffma"), y)     # deterministic
+
+
+def test_tree_with_c0(dev):
+    g = torch.Generator(device=dev).manual_seed(1)
+    x = torch.randn(512, 8192, device=dev, generator=g)
+    c0 = torch.randn(512, device=dev, generator=g)
+    y = contract("(i,j)->(i)", x, c0=c0, mode="ffma")
+    want = _want("(i,j)->(i)", [x], c0)
+    assert np.abs(y.double().cpu().numpy() - want).max() <= 1e-5 * np.abs(want).max()
+
+
+def test_tree_faster_than_exact_chain(dev):
+    """4096^2 full sum: the exact path is one dependent chain (reference
+    order); the tree uses the whole GPU."""
+    x = torch.randn(4096, 4096, device=dev)
+    for mode in ("exact", "ffma"):
+        contract("(i,j)->()", x, mode=mode)
+    torch.cuda.synchronize()
+    t = {}
+    for mode in ("exact", "ffma"):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        contract("(i,j)->()", x, mode=mode)
+        e.record()
+        torch.cuda.synchronize()
+        t[mode] = s.elapsed_time(e)
+    assert t["ffma"] * 20 < t["exact"], t
