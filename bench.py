@@ -52,6 +52,7 @@ CHAIN_FLOP_MINORDER = 2 * K_ * J_ * L_ + 2 * I_ * K_ * L_
 SPEC = "(i,k),(k,j),(j,l)->(i,l)"
 WORKLOAD = "chain (i,k),(k,j),(j,l)->(i,l) I=32768 K=J=L=8192 bf16 (BASELINE config 5)"
 METRIC = "contraction TFLOP/s and % tensor-core peak at 1/2/4/8 B200 vs CPU oracle"
+AUX_TIMEOUT_S = float(os.environ.get("BGX_AUX_TIMEOUT_S", "240"))
 
 
 def peaks():
@@ -715,45 +716,10 @@ def main():
         del Aw, Ow
         torch.cuda.empty_cache()
 
-    aux = None
     cpu = None
-    if not args.no_aux and (world == 1 or backend == "nccl"):
-        ok, why = True, ""
-        if world > 1:
-            # every rank must agree that symmetric memory works before any
-            # rank enters the fused path's collectives (no rank may be left
-            # waiting in a barrier the others never reach)
-            try:
-                from torch.distributed import _symmetric_memory as symm_mem
-                probe = symm_mem.empty(64, dtype=torch.uint8, device=dev)
-                symm_mem.rendezvous(probe, dist.group.WORLD)
-            except Exception as e:  # noqa: BLE001
-                ok, why = False, f"{type(e).__name__}: {e}"[:200]
-            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-            if int(flag.item()) == 0:
-                ok, why = False, why or "symmetric memory unavailable on another rank"
-        if ok:
-            try:
-                ks = ksplit_aux(dev, world, rank)
-            except Exception as e:  # an aux line must never sink the headline
-                ks = {"error": f"{type(e).__name__}: {e}"[:300]}
-        else:
-            ks = {"skipped": why}
-        aux = {"ksplit_fused_reduce_scatter": ks}
-    if rank == 0 and world == 1:
-        if not args.no_aux:
-            aux.update(aux_configs(dev, pk))
-            try:
-                aux["c4_f32_like_for_like"] = f32_aux(dev)
-            except Exception as e:  # noqa: BLE001
-                aux["c4_f32_like_for_like"] = {"error": f"{type(e).__name__}: {e}"[:300]}
-            opt = chain_optimal_order(dev)
-            opt["speedup_vs_left_to_right_time"] = ms / opt["ms"]
-            aux["c5_chain_min_flop_order"] = opt
-        if not args.no_cpu:
-            Bh, Ch = B.float().cpu().numpy(), C.float().cpu().numpy()
-            cpu = cpu_baseline(A[:1].float().cpu().numpy(), Bh, Ch)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        Bh, Ch = B.float().cpu().numpy(), C.float().cpu().numpy()
+        cpu = cpu_baseline(A[:1].float().cpu().numpy(), Bh, Ch)
     # the tile shape the library picked for the chain GEMMs (transparency)
     tile_info = None
     try:
@@ -778,38 +744,88 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get("bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (torch.randn on device, bf16-rounded)",
+        "config": {"workload": WORKLOAD, "I": total_rows, "I_per_rank": rows, "K": K_,
+                   "J": J_, "L": L_, "parallelism": f"M-shard x{world}",
+                   "order": "left-to-right (A@B)@C", "flop_per_step": job_flop,
+                   "flop_min_order": CHAIN_FLOP_MINORDER,
+                   "api": "paper_2503_04771_b200.contract(SPEC, A, B, C, out=O)",
+                   "l2": "inputs exceed L2 (A 512 MiB, A@B 512 MiB per 1-GPU step)"},
+        "fraction_of_peak": value / (pk["bf16"] * world),
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"],
+                     "unit": "TFLOP/s", "frac": achieved / pk["bf16"], "traffic": traffic,
+                     "kernel": "tc_gemm_kernel (tcgen05/TMEM/TMA)",
+                     "tile": tile_info,
+                     "flop_per_launch": gemm_flop, "launch_ms": gemm_ms,
+                     "peak_source": pk["source"] + " burst bf16",
+                     "frac_of_sustained": achieved / pk["bf16_sustained"],
+                     "frac_of_datasheet_2250": achieved / 2250.0},
+        "host_gap": {"kernel_ms_per_step": kernel_ms_per_step, "step_ms_rank0": ms_local,
+                     "gap_frac": max(0.0, 1 - kernel_ms_per_step / ms_local),
+                     "note": "device time between library launches inside contract() "
+                             "(planning, allocation, Python) as a fraction of the step"},
+        "parity": {"relF_row_samples_max_over_ranks": relF, "tolerance": 1e-2,
+                   "oracle": "float64 (A@B)@C on the bf16 inputs"},
+        "weak": weak,
+        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+        "clocks": clocks, "aux": None,
+    }
+
+    # aux lines: never allowed to sink or hang the headline.  A watchdog on
+    # every rank ends the process (exit 0) if they overrun; rank 0 then
+    # prints the headline with the aux marked as timed out.
+    done = threading.Event()
+
+    def watchdog():
+        if not done.wait(AUX_TIMEOUT_S):
+            if rank == 0:
+                line["aux"] = {"timeout": f"aux lines exceeded {AUX_TIMEOUT_S} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+    if not args.no_aux:
+        threading.Thread(target=watchdog, daemon=True).start()
+    aux = None
+    if not args.no_aux and (world == 1 or backend == "nccl"):
+        ok, why = True, ""
+        if world > 1:
+            # every rank must agree that symmetric memory works before any
+            # rank enters the fused path's collectives (no rank may be left
+            # waiting in a barrier the others never reach)
+            try:
+                from torch.distributed import _symmetric_memory as symm_mem
+                probe = symm_mem.empty(64, dtype=torch.uint8, device=dev)
+                symm_mem.rendezvous(probe, dist.group.WORLD)
+            except Exception as e:  # noqa: BLE001
+                ok, why = False, f"{type(e).__name__}: {e}"[:200]
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                ok, why = False, why or "symmetric memory unavailable on another rank"
+        if ok:
+            try:
+                ks = ksplit_aux(dev, world, rank)
+            except Exception as e:  # an aux line must never sink the headline
+                ks = {"error": f"{type(e).__name__}: {e}"[:300]}
+        else:
+            ks = {"skipped": why}
+        aux = {"ksplit_fused_reduce_scatter": ks}
+    if rank == 0 and world == 1 and not args.no_aux:
+        aux.update(aux_configs(dev, pk))
+        try:
+            aux["c4_f32_like_for_like"] = f32_aux(dev)
+        except Exception as e:  # noqa: BLE001
+            aux["c4_f32_like_for_like"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        opt = chain_optimal_order(dev)
+        opt["speedup_vs_left_to_right_time"] = ms / opt["ms"]
+        aux["c5_chain_min_flop_order"] = opt
+    done.set()
+    line["aux"] = aux
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic (torch.randn on device, bf16-rounded)",
-            "config": {"workload": WORKLOAD, "I": total_rows, "I_per_rank": rows, "K": K_,
-                       "J": J_, "L": L_, "parallelism": f"M-shard x{world}",
-                       "order": "left-to-right (A@B)@C", "flop_per_step": job_flop,
-                       "flop_min_order": CHAIN_FLOP_MINORDER,
-                       "api": "paper_2503_04771_b200.contract(SPEC, A, B, C, out=O)",
-                       "l2": "inputs exceed L2 (A 512 MiB, A@B 512 MiB per 1-GPU step)"},
-            "fraction_of_peak": value / (pk["bf16"] * world),
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["bf16"],
-                         "unit": "TFLOP/s", "frac": achieved / pk["bf16"], "traffic": traffic,
-                         "kernel": "tc_gemm_kernel (tcgen05/TMEM/TMA)",
-                         "tile": tile_info,
-                         "flop_per_launch": gemm_flop, "launch_ms": gemm_ms,
-                         "peak_source": pk["source"] + " burst bf16",
-                         "frac_of_sustained": achieved / pk["bf16_sustained"],
-                         "frac_of_datasheet_2250": achieved / 2250.0},
-            "host_gap": {"kernel_ms_per_step": kernel_ms_per_step, "step_ms_rank0": ms_local,
-                         "gap_frac": max(0.0, 1 - kernel_ms_per_step / ms_local),
-                         "note": "device time between library launches inside contract() "
-                                 "(planning, allocation, Python) as a fraction of the step"},
-            "parity": {"relF_row_samples_max_over_ranks": relF, "tolerance": 1e-2,
-                       "oracle": "float64 (A@B)@C on the bf16 inputs"},
-            "weak": weak,
-            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-            "clocks": clocks, "aux": aux,
-        }
-        print(json.dumps(line))
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

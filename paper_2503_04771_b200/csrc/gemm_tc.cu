@@ -53,6 +53,12 @@ namespace bgx {
 
 namespace {
 
+// Timeline probe (schedule debug bit 4096): %globaltimer when each CTA's
+// producer starts each of its first TR_UNITS units, read back with
+// bgxdbg_trace_read (A/B tooling, not part of the C ABI).
+constexpr int TR_CTAS = 160, TR_UNITS = 64;
+__device__ unsigned long long g_trace[TR_CTAS * TR_UNITS];
+
 constexpr int BM = 128;                     // rows of A per CTA
 constexpr int ROW_BYTES = 128;              // one 128B-swizzle row of K per k-block
 constexpr int A_STAGE_BYTES = BM * ROW_BYTES;  // 16 KB
@@ -405,7 +411,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
     int stage = 0;
     uint32_t phase = 0;
+    int trace_i = 0;
     for (int64_t u = cluster_id; u < p.num_units; u += num_clusters) {
+      if ((p.debug & 4096) && lane == 0 && blockIdx.x < TR_CTAS && trace_i < TR_UNITS) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[blockIdx.x * TR_UNITS + trace_i] = t;
+      }
+      ++trace_i;
       const UnitInfo ui = unit_info(p, u);
       const int64_t t = ui.t;
       const int kb_lo = ui.kb_lo, kb_hi = ui.kb_lo + ui.nkb;
@@ -1629,3 +1642,8 @@ void tc_tile_choice(const bgx_contract_desc &d, int *cg_out, int *bn_out) {
 }
 
 }  // namespace bgx
+
+extern "C" __attribute__((visibility("default"))) int bgxdbg_trace_read(void *host, int64_t bytes) {
+  const int64_t n = (int64_t)sizeof(bgx::g_trace) < bytes ? (int64_t)sizeof(bgx::g_trace) : bytes;
+  return cudaMemcpyFromSymbol(host, bgx::g_trace, (size_t)n) == cudaSuccess ? 0 : -3;
+}
