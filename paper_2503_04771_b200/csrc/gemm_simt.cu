@@ -69,8 +69,12 @@ simt_gemm_kernel(const Params p) {
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int LA = BM * KT / NT, LB = BN * KT / NT;   // elements per thread per tile
   static_assert(LA * NT == BM * KT && LB * NT == BN * KT, "tile / thread mismatch");
+  // B rows unpadded when each thread reads 4 consecutive f32 columns: one
+  // 16-byte shared load instead of four (8 lanes cover a 128-byte row, no
+  // bank conflict); padded otherwise
+  constexpr int BPAD = (TN % 4 == 0 && sizeof(Acc) == 4) ? 0 : 1;
   __shared__ Acc As[KT][BM + 1];
-  __shared__ Acc Bs[KT][BN + 1];
+  __shared__ __align__(16) Acc Bs[KT][BN + BPAD];
   const int tid = threadIdx.x;
   const int tx = tid % (BN / TN), ty = tid / (BN / TN);
   int64_t t = blockIdx.x;
@@ -138,12 +142,21 @@ simt_gemm_kernel(const Params p) {
     __syncthreads();
     if (k0 + KT < p.K) load(k0 + KT);    // in flight while this tile is multiplied
     const int kmax = (p.K - k0) < KT ? (int)(p.K - k0) : KT;
+#pragma unroll 8
     for (int kk = 0; kk < kmax; ++kk) {
       Acc av[TM], bv[TN];
 #pragma unroll
       for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+      if constexpr (BPAD == 0) {
 #pragma unroll
-      for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+        for (int j = 0; j < TN; j += 4) {
+          const float4 q = *reinterpret_cast<const float4 *>(&Bs[kk][tx * TN + j]);
+          bv[j] = q.x; bv[j + 1] = q.y; bv[j + 2] = q.z; bv[j + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+      }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -466,7 +479,17 @@ int launch(const bgx_contract_desc &d, cudaStream_t s) {
   const int sms = sm_count_current();
   const int64_t outs = d.M * d.N * d.batch;
   const bool small = outs < (int64_t)sms * 64 * 64 * 2;
-  if (outs <= (int64_t)sms * 2048) {
+  // BGX_SIMT_SMALL (A/B only): 0 = one output per thread, 1 = four chains per thread
+  static const int small_variant = getenv("BGX_SIMT_SMALL") ? atoi(getenv("BGX_SIMT_SMALL")) : 1;
+  const int64_t tiles_16x32 = ((d.M + 15) / 16) * ((d.N + 31) / 32) * d.batch;
+  if (outs <= (int64_t)sms * 2048 && small_variant == 1 && tiles_16x32 >= sms / 2) {
+    // latency-bound sizes: the per-output k-sequential chain is the floor;
+    // four independent chains per thread (1 x 4 outputs) hide the add
+    // latency and amortise the shared-memory reads, 16 x 32 tiles of 128
+    // threads keep one block on (almost) every SM
+    p.tiles_m = (d.M + 15) / 16; p.tiles_n = (d.N + 31) / 32;
+    simt_gemm_kernel<In, Out, Acc, FUSED, 16, 32, 1, 4, 64><<<(unsigned)tiles_16x32, 128, 0, s>>>(p);
+  } else if (outs <= (int64_t)sms * 2048) {
     // latency-bound sizes: one output per thread, 16 x 16 tiles (the per-output
     // k-sequential chain is the floor, so maximise the number of chains)
     p.tiles_m = (d.M + 15) / 16; p.tiles_n = (d.N + 15) / 16;
