@@ -136,15 +136,20 @@ transpose_vec_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t nx, 
 }
 
 // ---- row copy ---------------------------------------------------------------
-// Rows of length n along a dim that is inner in both tensors.
+// Rows of length n along a dim that is inner in both tensors.  Long rows are
+// cut into `nchunk` pieces of `chunk` elements, one per block, so a single
+// contiguous run (an identity permutation, or any copy whose dims all merge)
+// still spreads over every SM.
 template <typename T>
 __global__ void __launch_bounds__(256)
 copy_rows_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t n, int64_t in_s,
-                 int64_t out_s, int64_t rows, BatchDims bd) {
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+                 int64_t out_s, int64_t rows, int64_t chunk, int64_t nchunk, BatchDims bd) {
+  for (int64_t blk = blockIdx.x; blk < rows * nchunk; blk += gridDim.x) {
+    const int64_t r = blk / nchunk, c0 = (blk % nchunk) * chunk;
+    const int64_t c1 = c0 + chunk < n ? c0 + chunk : n;
     int64_t in_off, out_off;
     decode_batch(bd, r, in_off, out_off);
-    for (int64_t x = threadIdx.x; x < n; x += blockDim.x)
+    for (int64_t x = c0 + threadIdx.x; x < c1; x += blockDim.x)
       out[out_off + x * out_s] = in[in_off + x * in_s];
   }
 }
@@ -152,22 +157,24 @@ copy_rows_kernel(const T *__restrict__ in, T *__restrict__ out, int64_t n, int64
 // Contiguous rows, 16-byte vectors (rows and bases 16B aligned).
 __global__ void __launch_bounds__(256)
 copy_rows_vec_kernel(const uint4 *__restrict__ in, uint4 *__restrict__ out, int64_t nvec,
-                     int64_t rows, BatchDims bd) {
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+                     int64_t rows, int64_t chunk, int64_t nchunk, BatchDims bd) {
+  for (int64_t blk = blockIdx.x; blk < rows * nchunk; blk += gridDim.x) {
+    const int64_t r = blk / nchunk, c0 = (blk % nchunk) * chunk;
+    const int64_t c1 = c0 + chunk < nvec ? c0 + chunk : nvec;
     int64_t in_off, out_off;
     decode_batch(bd, r, in_off, out_off);  // in uint4 units (host pre-divides)
     const uint4 *src = in + in_off;
     uint4 *dst = out + out_off;
-    int64_t x = threadIdx.x;
-    for (; x + 3 * 256 < nvec; x += 4 * 256) {
-      uint4 v0 = __ldcs(src + x), v1 = __ldcs(src + x + 256), v2 = __ldcs(src + x + 512),
-            v3 = __ldcs(src + x + 768);
-      __stcs(dst + x, v0);
-      __stcs(dst + x + 256, v1);
-      __stcs(dst + x + 512, v2);
-      __stcs(dst + x + 768, v3);
+    int64_t x = c0 + threadIdx.x;
+    constexpr int U = 8;   // 8 independent 16-byte loads in flight per thread
+    for (; x + (U - 1) * 256 < c1; x += U * 256) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldcs(src + x + u * 256);
+#pragma unroll
+      for (int u = 0; u < U; ++u) __stcs(dst + x + u * 256, v[u]);
     }
-    for (; x < nvec; x += 256) __stcs(dst + x, __ldcs(src + x));
+    for (; x < c1; x += 256) __stcs(dst + x, __ldcs(src + x));
   }
 }
 
@@ -201,18 +208,23 @@ int launch_permute(const void *in, void *out, std::vector<Dim> dims, cudaStream_
                   ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0);
     for (int d = 0; d < bd.n && vec_ok; ++d)
       vec_ok = bd.in_stride[d] % vec == 0 && bd.out_stride[d] % vec == 0;
-    int64_t grid = std::min<int64_t>(rows, (int64_t)sms * 32);
+    // rows cut into 2048-element (vector) pieces handed out grid-stride, so
+    // the blocks in flight stream one contiguous window of memory
+    const int64_t len = vec_ok ? row.extent / vec : row.extent;
+    const int64_t chunk = len < 2048 ? (len > 0 ? len : 1) : 2048;
+    const int64_t nchunk = (len + chunk - 1) / chunk;
+    int64_t grid = std::min<int64_t>(rows * nchunk, (int64_t)sms * 32);
     if (vec_ok) {
       for (int d = 0; d < bd.n; ++d) {
         bd.in_stride[d] /= vec;
         bd.out_stride[d] /= vec;
       }
       copy_rows_vec_kernel<<<(unsigned)grid, 256, 0, s>>>((const uint4 *)in, (uint4 *)out,
-                                                         row.extent / vec, rows, bd);
+                                                         len, rows, chunk, nchunk, bd);
     } else {
       copy_rows_kernel<T><<<(unsigned)grid, 256, 0, s>>>((const T *)in, (T *)out, row.extent,
                                                          row.in_stride, row.out_stride, rows,
-                                                         bd);
+                                                         chunk, nchunk, bd);
     }
     return check_launch("permute copy");
   }

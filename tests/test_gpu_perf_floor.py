@@ -42,3 +42,26 @@ def test_permute_floor(dev):
     ms = _ms(lambda: contract("(i,j)->(j,i)", x, out=out))
     gbs = 2 * x.numel() * 4 / ms / 1e6
     assert gbs >= 4000.0, f"transpose {gbs:.0f} GB/s < 4000"
+
+
+@pytest.mark.parametrize("spec,shape", [("(i,j)->(i,j)", (8192, 8192)),
+                                        ("(i)->(i)", (1 << 26,)),
+                                        ("(i,j,k)->(i,j,k)", (64, 1024, 1024))])
+def test_identity_copy_floor(dev, spec, shape):
+    """Passthrough bodies whose dims all merge into one contiguous run (round
+    2 fix: that run was copied by ONE block, ~53 GB/s) spread over every SM."""
+    x = torch.randn(shape, device=dev)
+    out = torch.empty_like(x)
+    ms = _ms(lambda: contract(spec, x, out=out))
+    gbs = 2 * x.numel() * 4 / ms / 1e6
+    assert torch.equal(out, x)
+    assert gbs >= 3000, f"{spec}: {gbs:.0f} GB/s"
+
+
+@pytest.mark.parametrize("n", [1, 7, 4095, 4097, 1 << 20, (1 << 20) + 3])
+def test_long_row_copy_chunks_exact(dev, n):
+    """Chunked row copies: every element lands once, vector and scalar paths."""
+    x = torch.randn(n, device=dev)
+    assert torch.equal(contract("(i)->(i)", x), x)
+    y = torch.randn(3, n, device=dev)[:, : max(1, n - 1)]     # unaligned rows: scalar path
+    assert torch.equal(contract("(b,i)->(b,i)", y), y)
