@@ -141,6 +141,44 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
   }
 }
 
+// Dense elementwise bodies (Hadamard products: every input strided like the
+// row-major output, no reduction): 16-byte vectors of every operand per
+// thread, the same per-element arithmetic as generic_kernel (left-fold
+// product, + c0 or +0.0, separately rounded) — bit-identical, HBM-bound.
+template <typename S, typename T, int NIN>
+__global__ void __launch_bounds__(256)
+dense_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
+  constexpr int V = 16 / (int)sizeof(S);
+  const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+  const S *c0 = static_cast<const S *>(d.c0);
+  S *out = static_cast<S *>(d.out);
+  const int64_t nv = n_out / V;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    uint4 q[NIN + 1];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) q[k] = __ldcs(reinterpret_cast<const uint4 *>(ins[k]) + i);
+    q[NIN] = c0 ? __ldcs(reinterpret_cast<const uint4 *>(c0) + i) : make_uint4(0, 0, 0, 0);
+    uint4 r;
+    S *re = reinterpret_cast<S *>(&r);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      T p = ld_as<S, T>(reinterpret_cast<const S *>(&q[0]) + e);
+#pragma unroll
+      for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, ld_as<S, T>(reinterpret_cast<const S *>(&q[k]) + e));
+      const T acc = c0 ? ld_as<S, T>(reinterpret_cast<const S *>(&q[NIN]) + e) : T(0);
+      re[e] = st_as<S, T>(add_rn<T>(p, acc));
+    }
+    __stcs(reinterpret_cast<uint4 *>(out) + i, r);
+  }
+  for (int64_t o = nv * V + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n_out; o += stride) {
+    T p = ld_as<S, T>(ins[0] + o);
+#pragma unroll
+    for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, ld_as<S, T>(ins[k] + o));
+    out[o] = st_as<S, T>(add_rn<T>(p, c0 ? ld_as<S, T>(c0 + o) : T(0)));
+  }
+}
+
 template <typename S, typename T, bool DENSE>
 void launch_generic_n(const bgx_generic_desc &d, int64_t n_out, int64_t red, unsigned blocks,
                       cudaStream_t s) {
@@ -453,6 +491,18 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
     static const bool no_rr = getenv("BGX_NO_ROWREDUCE") != nullptr;
     if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
     if (!no_rr && try_chain<T>(d, n_out, red, s, &rc)) return rc;
+  }
+  if (dense && d.n_in >= 2 && d.n_in <= 3 && red == 1) {
+    bool aligned = ((uintptr_t)d.out % 16 == 0) && ((uintptr_t)d.c0 % 16 == 0);
+    for (int k = 0; k < d.n_in; ++k) aligned = aligned && ((uintptr_t)d.ins[k] % 16 == 0);
+    if (aligned) {
+      int64_t vb = (n_out / (16 / (int64_t)sizeof(S)) + 255) / 256;
+      if (vb > (int64_t)sms * 16) vb = (int64_t)sms * 16;
+      if (vb < 1) vb = 1;
+      if (d.n_in == 2) dense_ew_kernel<S, T, 2><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+      else dense_ew_kernel<S, T, 3><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+      return check_launch("dense_ew_kernel");
+    }
   }
   if (dense) launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);
   else launch_generic_n<S, T, false>(d, n_out, red, (unsigned)blocks, s);

@@ -20,6 +20,7 @@ namespace {
 
 constexpr int TR_THREADS = 256;
 constexpr int64_t TR_MIN_CHUNK = 2048;   // points per block at least
+constexpr int64_t TR_WARP_MAX = 8192;    // contiguous runs up to this: one warp per output
 
 template <typename S, typename T> __device__ __forceinline__ T ld_t(const S *p) {
   return (T)Conv<S>::to_f(*p);
@@ -217,6 +218,59 @@ tree_contig_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red, int spl
   }
 }
 
+// CONTIG layout with short runs (a block per output would leave most of its
+// threads idle): one WARP per output, 16-byte vectors per lane, shuffle sum.
+template <typename S, typename T, int NIN>
+__global__ void __launch_bounds__(TR_THREADS)
+tree_contig_warp_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red) {
+  constexpr int V = Vec<S, T>::N;
+  const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * (TR_THREADS / 32);
+  for (int64_t o = (int64_t)blockIdx.x * (TR_THREADS / 32) + threadIdx.x / 32; o < n_out;
+       o += warps) {
+    int64_t base[BGX_MAX_OPERANDS];
+    par_offsets(d, o, NIN, base);
+    const S *p[NIN];
+    bool aligned = true;
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      p[k] = ins[k] + base[k];
+      aligned = aligned && ((uintptr_t)p[k] % 16 == 0);
+    }
+    T acc = 0;
+    int64_t done = 0;
+    if (aligned) {
+      const int64_t nv = red / V;
+      for (int64_t i = lane; i < nv; i += 32) {
+        T v[NIN][V];
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) Vec<S, T>::load(p[k] + i * V, v[k]);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          T q = v[0][e];
+#pragma unroll
+          for (int k = 1; k < NIN; ++k) q *= v[k][e];
+          acc += q;
+        }
+      }
+      done = nv * V;
+    }
+    for (int64_t i = done + lane; i < red; i += 32) {
+      T q = ld_t<S, T>(p[0] + i);
+#pragma unroll
+      for (int k = 1; k < NIN; ++k) q *= ld_t<S, T>(p[k] + i);
+      acc += q;
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+    if (lane == 0) {
+      if (d.c0) acc += ld_t<S, T>(static_cast<const S *>(d.c0) + o);
+      static_cast<S *>(d.out)[o] = st_t<S, T>(acc);
+    }
+  }
+}
+
 // COLUMN layout: the innermost OUTPUT axis has unit stride (or is broadcast)
 // in every input and the reduction runs across it (column sums, x^T A): a
 // block owns 32 consecutive outputs along that axis — one per lane, so each
@@ -234,8 +288,10 @@ tree_column_kernel(const bgx_generic_desc d, int64_t n_tiles, int64_t red, int s
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
   for (int64_t blk = blockIdx.x; blk < n_tiles * splits; blk += gridDim.x) {
-    const int64_t t = blk / splits;
-    const int s = (int)(blk % splits);
+    // tile fastest: the blocks in flight read adjacent 128-byte segments of
+    // the same rows (DRAM row locality), chunk by chunk
+    const int64_t t = blk % n_tiles;
+    const int s = (int)(blk / n_tiles);
     const int64_t q = t / ctiles, c = (t % ctiles) * 32 + lane;
     const bool live = c < E;
     int64_t base[BGX_MAX_OPERANDS];
@@ -249,10 +305,13 @@ tree_column_kernel(const bgx_generic_desc d, int64_t n_tiles, int64_t red, int s
 #pragma unroll
       for (int k = 0; k < NIN; ++k) base[k] += i * d.strides[k][a];
     }
-    const int64_t lo = (int64_t)s * chunk;
-    const int64_t hi = lo + chunk < red ? lo + chunk : red;
     T acc = 0;
     constexpr int W = TR_THREADS / 32;
+    // chunks s, s + splits, ...: the blocks in flight move down the rows
+    // together (a narrow window of rows, i.e. of DRAM pages and TLB entries)
+    for (int64_t cb = (int64_t)s * chunk; cb < red; cb += (int64_t)splits * chunk) {
+    const int64_t lo = cb;
+    const int64_t hi = lo + chunk < red ? lo + chunk : red;
     if (n_red == 1) {
       // one reduction axis: point r at base + r * stride; U points of every
       // warp in flight at once
@@ -302,6 +361,7 @@ tree_column_kernel(const bgx_generic_desc d, int64_t n_tiles, int64_t red, int s
         }
       }
     }
+    }   // chunks
     part[w][lane] = acc;
     __syncthreads();
     if (w == 0 && live) {
@@ -314,6 +374,111 @@ tree_column_kernel(const bgx_generic_desc d, int64_t n_tiles, int64_t red, int s
         static_cast<S *>(d.out)[o] = st_t<S, T>(sum);
       } else {
         ws[o * splits + s] = sum;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// COLUMN layout, 16-bit storage, one reduction axis, even column count:
+// each lane owns TWO adjacent columns (one 4-byte load per input per point),
+// so a warp row is 64 columns = one 128-byte line, as for f32.  BCM: bit k
+// set = input k is broadcast along the columns (stride 0, one scalar per
+// point) — a template parameter, so the unrolled loads stay branch-free.
+template <typename S, int NIN, int BCM>
+__global__ void __launch_bounds__(TR_THREADS)
+tree_column2_kernel(const bgx_generic_desc d, int64_t n_tiles, int64_t red, int splits,
+                    int64_t chunk, float *ws) {
+  __shared__ float part[TR_THREADS / 32][64];
+  const int pl = d.n_par - 1;
+  const int64_t E = d.extents[pl];
+  const int64_t ctiles = (E + 63) / 64;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int W = TR_THREADS / 32;
+  const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+  for (int64_t blk = blockIdx.x; blk < n_tiles * splits; blk += gridDim.x) {
+    const int64_t t = blk % n_tiles;
+    const int s = (int)(blk / n_tiles);
+    const int64_t q = t / ctiles, c = (t % ctiles) * 64 + 2 * lane;
+    const bool live = c < E;                   // E even: c + 1 < E too
+    const S *ptr[NIN];
+    int64_t st[NIN];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      int64_t off = ((BCM >> k) & 1) ? 0 : (live ? c : 0);
+      int64_t rem = q;
+      for (int a = pl - 1; a >= 0; --a) {
+        const int64_t e = d.extents[a];
+        off += (rem % e) * d.strides[k][a];
+        rem /= e;
+      }
+      ptr[k] = ins[k] + off;
+      st[k] = d.strides[k][d.n_par];
+    }
+    float a0 = 0.f, a1 = 0.f;
+    for (int64_t cb = (int64_t)s * chunk; cb < red && live; cb += (int64_t)splits * chunk) {
+      const int64_t hi = cb + chunk < red ? cb + chunk : red;
+      constexpr int U = 8;
+      int64_t r = cb + w;
+      for (; r + (U - 1) * W < hi; r += U * W) {
+        float x0[U], x1[U];
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const S *pp = ptr[k] + (r + u * W) * st[k];
+            float v0, v1;
+            if ((BCM >> k) & 1) {   // folded after unrolling
+              v0 = v1 = Conv<S>::to_f(*pp);
+            } else {
+              const uint32_t two = *reinterpret_cast<const uint32_t *>(pp);
+              const S *e = reinterpret_cast<const S *>(&two);
+              v0 = Conv<S>::to_f(e[0]);
+              v1 = Conv<S>::to_f(e[1]);
+            }
+            if (k == 0) { x0[u] = v0; x1[u] = v1; } else { x0[u] *= v0; x1[u] *= v1; }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) { a0 += x0[u]; a1 += x1[u]; }
+      }
+      for (; r < hi; r += W) {
+        float x0 = 1.f, x1 = 1.f;
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) {
+          const S *pp = ptr[k] + r * st[k];
+          float v0, v1;
+          if ((BCM >> k) & 1) {   // folded after unrolling
+            v0 = v1 = Conv<S>::to_f(*pp);
+          } else {
+            const uint32_t two = *reinterpret_cast<const uint32_t *>(pp);
+            const S *e = reinterpret_cast<const S *>(&two);
+            v0 = Conv<S>::to_f(e[0]);
+            v1 = Conv<S>::to_f(e[1]);
+          }
+          if (k == 0) { x0 = v0; x1 = v1; } else { x0 *= v0; x1 *= v1; }
+        }
+        a0 += x0;
+        a1 += x1;
+      }
+    }
+    part[w][2 * lane] = a0;
+    part[w][2 * lane + 1] = a1;
+    __syncthreads();
+    if (w < 2) {
+      const int col = w * 32 + lane;           // 64 columns over two warps
+      const int64_t cc = (t % ctiles) * 64 + col;
+      if (cc < E) {
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) sum += part[j][col];
+        const int64_t o = q * E + cc;
+        if (splits == 1) {
+          if (d.c0) sum += Conv<S>::to_f(static_cast<const S *>(d.c0)[o]);
+          static_cast<S *>(d.out)[o] = Conv<S>::from_f(sum);
+        } else {
+          ws[o * splits + s] = sum;
+        }
       }
     }
     __syncthreads();
@@ -333,7 +498,7 @@ tree_finish_kernel(const bgx_generic_desc d, int64_t n_out, int splits, const T 
   }
 }
 
-enum class TreeLayout { General, Contig, Column };
+enum class TreeLayout { General, Contig, Column, Column2 };
 
 // Which kernel fits the operand layout (see the kernels above).
 TreeLayout tree_layout(const bgx_generic_desc &d) {
@@ -353,7 +518,19 @@ TreeLayout tree_layout(const bgx_generic_desc &d) {
       if (d.strides[k][pl] == 1) col = true;
       else if (d.strides[k][pl] != 0) ok = false;
     }
-    if (ok && col) return TreeLayout::Column;
+    if (ok && col) {
+      // 16-bit, one reduction axis, every unit-stride input 4-byte aligned
+      // at even columns: two columns per lane
+      bool two = dtype_size(d.dtype) == 2 && d.n_axes - d.n_par == 1 && d.n_in <= 2 &&
+                 d.extents[pl] % 2 == 0;
+      for (int k = 0; k < d.n_in && two; ++k) {
+        if (d.strides[k][pl] == 0) continue;
+        two = ((uintptr_t)d.ins[k] % 4 == 0);
+        for (int a = 0; a < d.n_axes && two; ++a)
+          if (a != pl && d.extents[a] != 1) two = d.strides[k][a] % 2 == 0;
+      }
+      return two ? TreeLayout::Column2 : TreeLayout::Column;
+    }
   }
   return TreeLayout::General;
 }
@@ -362,16 +539,18 @@ TreeLayout tree_layout(const bgx_generic_desc &d) {
 // column tiles), and the chunk count per unit: enough blocks to fill the
 // GPU (8 per SM), each chunk at least TR_MIN_CHUNK points.
 int64_t tree_units(const bgx_generic_desc &d, TreeLayout lay, int64_t n_out) {
-  if (lay != TreeLayout::Column) return n_out;
+  if (lay != TreeLayout::Column && lay != TreeLayout::Column2) return n_out;
   const int64_t E = d.extents[d.n_par - 1];
-  return (n_out / E) * ((E + 31) / 32);
+  const int64_t cw = lay == TreeLayout::Column2 ? 64 : 32;
+  return (n_out / E) * ((E + cw - 1) / cw);
 }
 
 int tree_splits(int64_t units, int64_t red, TreeLayout lay) {
   const int sms = sm_count_current();
   const int64_t target = (int64_t)(sms > 0 ? sms : 148) * 8;   // 8 blocks of 256 per SM
   int64_t sp = (target + units - 1) / units;
-  const int64_t min_chunk = lay == TreeLayout::Column ? 256 : TR_MIN_CHUNK;
+  const int64_t min_chunk =
+      (lay == TreeLayout::Column || lay == TreeLayout::Column2) ? 256 : TR_MIN_CHUNK;
   const int64_t by_size = (red + min_chunk - 1) / min_chunk;
   if (sp > by_size) sp = by_size;
   if (sp > 65536) sp = 65536;
@@ -387,6 +566,9 @@ int launch_tree(const bgx_generic_desc &d, int64_t n_out, int64_t red, void *ws,
   const int splits = tree_splits(units, red, lay);
   int64_t chunk = (red + splits - 1) / splits;
   if (lay == TreeLayout::Contig) chunk = (chunk + 63) / 64 * 64;   // keeps 16-byte vector runs aligned
+  // column layouts: `splits` partial sums per output, each over the
+  // interleaved 256-row chunks s, s + splits, ...
+  if (lay == TreeLayout::Column || lay == TreeLayout::Column2) chunk = 256;
   if (splits > 1 && (ws == nullptr || ws_bytes < n_out * splits * (int64_t)sizeof(T))) {
     set_error("bgx_generic_tree: workspace of %lld bytes needed",
               (long long)(n_out * splits * (int64_t)sizeof(T)));
@@ -404,8 +586,32 @@ int launch_tree(const bgx_generic_desc &d, int64_t n_out, int64_t red, void *ws,
     case 2: KERN<S, T, 2><<<g, TR_THREADS, 0, s>>>(d, ARG0, red, splits, chunk, w); break;  \
     default: KERN<S, T, 3><<<g, TR_THREADS, 0, s>>>(d, ARG0, red, splits, chunk, w); break; \
   }
+  if (lay == TreeLayout::Contig && splits == 1 && red <= TR_WARP_MAX) {
+    int64_t wb = (n_out + TR_THREADS / 32 - 1) / (TR_THREADS / 32);
+    if (wb > cap) wb = cap;
+    switch (d.n_in) {
+      case 1: tree_contig_warp_kernel<S, T, 1><<<(unsigned)wb, TR_THREADS, 0, s>>>(d, n_out, red); break;
+      case 2: tree_contig_warp_kernel<S, T, 2><<<(unsigned)wb, TR_THREADS, 0, s>>>(d, n_out, red); break;
+      default: tree_contig_warp_kernel<S, T, 3><<<(unsigned)wb, TR_THREADS, 0, s>>>(d, n_out, red); break;
+    }
+    return check_launch("tree_contig_warp_kernel");
+  }
   if (lay == TreeLayout::Contig) {
     BGX_TREE_LAUNCH(tree_contig_kernel, n_out)
+  } else if (lay == TreeLayout::Column2) {
+    if constexpr (sizeof(S) == 2) {
+      float *wf = reinterpret_cast<float *>(w);
+      const int pl = d.n_par - 1;
+      const int bcm = (d.strides[0][pl] == 0 ? 1 : 0) | (d.n_in > 1 && d.strides[1][pl] == 0 ? 2 : 0);
+      if (d.n_in == 1)
+        tree_column2_kernel<S, 1, 0><<<g, TR_THREADS, 0, s>>>(d, units, red, splits, chunk, wf);
+      else if (bcm == 1)
+        tree_column2_kernel<S, 2, 1><<<g, TR_THREADS, 0, s>>>(d, units, red, splits, chunk, wf);
+      else if (bcm == 2)
+        tree_column2_kernel<S, 2, 2><<<g, TR_THREADS, 0, s>>>(d, units, red, splits, chunk, wf);
+      else
+        tree_column2_kernel<S, 2, 0><<<g, TR_THREADS, 0, s>>>(d, units, red, splits, chunk, wf);
+    }
   } else if (lay == TreeLayout::Column) {
     BGX_TREE_LAUNCH(tree_column_kernel, units)
   } else {

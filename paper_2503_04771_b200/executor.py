@@ -315,6 +315,7 @@ def _launch(lib, d, kind, splits, ws_bytes, out) -> int:
 
 
 PAD_MIN_FLOP = 1 << 28
+TREE_16BIT_POINTS = 1024
 
 
 def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0,
@@ -551,7 +552,17 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
             _cache_put(_exec_cache(), key, _fast_permute(inputs[0], out, plan.perm))
         return out
     if isinstance(plan, GenericPlan):
-        tree = mode == "ffma"    # tolerance mode: tree reductions
+        # tolerance mode: tree reductions; 16-bit storage (no reference
+        # arithmetic to reproduce) also takes them once each output sums
+        # TREE_16BIT_POINTS or more points — shorter reductions keep the
+        # sequential f32 chain (bit-equal to the oracle on widened inputs)
+        tree = mode == "ffma"
+        if not tree and mode == "auto" and dt in (torch.bfloat16, torch.float16):
+            red_pts = 1
+            for a, e in extents_of(spec, [t.shape for t in inputs] + [out.shape]).items():
+                if a not in spec.output:
+                    red_pts *= e
+            tree = red_pts >= TREE_16BIT_POINTS
         if out.is_contiguous():
             return generic(spec, inputs, c0, out, tree=tree)
         tmp = torch.empty(out.shape, dtype=dt, device=out.device)

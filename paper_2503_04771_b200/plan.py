@@ -191,6 +191,8 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
     ref_types = dtype in ("f32", "f64")
     if n_in == 1:
         return GenericPlan("single-input reduction")
+    if n_in >= 3 and all_par:
+        return GenericPlan("elementwise product (no reduction)")
     if n_in >= 3:
         points = _prod(ext[a] for a in spec.axes)
         if ref_types and mode in ("auto", "exact"):
@@ -203,8 +205,19 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
     if isinstance(groups, str):
         return GenericPlan(groups)
     batch, m, n, k = groups
-    if ref_types and not k and (not m or not n):
+    if not k and (not m or not n):
+        # Hadamard-type bodies (no reduction, no M x N structure): a GEMM plan
+        # would be batch x 1 x 1 x 1 (round 2: a 16-bit 8192^2 Hadamard took
+        # 2 s on the SIMT GEMM); the dense/strided elementwise kernels move
+        # the bytes at HBM speed.  16-bit: f32 arithmetic, one final rounding
+        # (the GEMM path's semantics).  Outer products (M x N, K = 1) stay
+        # GEMMs: their tiles write the output at full width.
         return GenericPlan("elementwise product (no reduction)")
+    if not ref_types and (_prod(ext[a] for a in m) == 1 or _prod(ext[a] for a in n) == 1):
+        # 16-bit matrix-vector / batched dot products: a GEMM with one live
+        # row or column per tile (or batch x 1 x 1 x K) wastes the tensor
+        # cores; reductions on the generic path (tree sums when long)
+        return GenericPlan("matrix-vector / dot products (16-bit)")
     if mode == "ffma" and k and (_prod(ext[a] for a in m) == 1 or _prod(ext[a] for a in n) == 1):
         # tolerance mode: dot products and matrix-vector bodies are block-wide
         # tree reductions (bgx_generic_tree), not GEMM tiles with one live

@@ -97,3 +97,13 @@ def test_reference_dtypes_stay_exact_at_any_size():
             assert isinstance(plan_of("(i,k),(k,j),(j,l)->(i,l)", ext, dtype=dt, mode=mode),
                               P.ChainPlan)
     assert isinstance(plan_of("(i,k),(k,j),(j,l)->(i,l)", ext, dtype="bf16"), P.ChainPlan)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "f32", "f64"])
+@pytest.mark.parametrize("text", ["(i,j),(i,j)->(i,j)", "(i,j),(i,j),(i,j)->(i,j)",
+                                  "(b,i),(b,i)->(b,i)", "(i,j),(j)->(i,j)"])
+def test_hadamard_bodies_are_elementwise_not_gemm(text, dtype):
+    """Round 2: 16-bit Hadamard bodies planned as a batch x 1 x 1 x 1 GEMM
+    (8192^2 bf16 took 2 s); every dtype now takes the elementwise kernels."""
+    p = plan_of(text, dict(i=8192, j=8192, b=8, k=1), dtype=dtype)
+    assert isinstance(p, P.GenericPlan), p
