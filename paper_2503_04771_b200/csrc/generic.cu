@@ -213,6 +213,11 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem, bool pre
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(smem)),
                "l"(gmem), "r"(sz) : "memory");
 }
+// 16-byte copy of the first `bytes` (0..16) bytes, the rest zero-filled.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -221,8 +226,19 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
 // COLS: the reduction axis is NOT contiguous but consecutive outputs are
 // (column sums, vector-matrix products): tile[step][lane] is then loaded
 // straight along the outputs — one coalesced line per reduction step.
-template <typename T, int NIN, bool COLS>
-__global__ void __launch_bounds__(32 * RR_WARPS)
+// VEC (row layout, 16-byte aligned rows): tiles are staged with 16-byte
+// cp.async — 32 / (row bytes / 16) rows per instruction instead of one — into
+// rows padded to a 16-byte multiple, and each lane folds its row from
+// 16-byte shared loads (conflict-free: 8 lanes per phase hit 8 distinct
+// 4-bank groups).  Same element order, same arithmetic.
+template <typename T> constexpr int rr_stride(bool vec, int tj = RR_TJ) {
+  return vec ? tj + 16 / (int)sizeof(T) : tj + 1;
+}
+
+// NW warps per block, ST tiles in flight per warp, TJ columns per tile.
+template <typename T, int NIN, bool COLS, bool VEC = false, int NW = RR_WARPS, int ST = RR_STAGES,
+          int TJ = RR_TJ>
+__global__ void __launch_bounds__(32 * NW)
 rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) {
   // shared_mask bit k: input k does not depend on the output index (e.g. the
   // vector of a GEMV): its tile row is loaded once and read by every lane
@@ -230,11 +246,12 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
   extern __shared__ __align__(16) uint8_t rr_smem_raw[];
   T *tiles = reinterpret_cast<T *>(rr_smem_raw);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  constexpr int TSZ = 32 * (RR_TJ + 1);          // one tile
-  T *wtiles = tiles + (size_t)warp * RR_STAGES * NIN * TSZ;
+  constexpr int RS = rr_stride<T>(VEC, TJ);          // tile row stride (elements)
+  constexpr int TSZ = 32 * RS;                    // one tile
+  T *wtiles = tiles + (size_t)warp * ST * NIN * TSZ;
   const int n_par = d.n_par;
   const int64_t E = d.extents[d.n_axes - 1];
-  const int64_t o0 = ((int64_t)blockIdx.x * RR_WARPS + warp) * 32;
+  const int64_t o0 = ((int64_t)blockIdx.x * NW + warp) * 32;
   if (o0 >= n_out) return;
   const int64_t o = o0 + lane;
   const bool row_ok = o < n_out;
@@ -253,10 +270,10 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     }
   }
   const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
-  const int64_t ntiles = (E + RR_TJ - 1) / RR_TJ;
+  const int64_t ntiles = (E + TJ - 1) / TJ;
   auto issue = [&](int64_t t) {
-    const int stage = (int)(t % RR_STAGES);
-    const int64_t j = t * RR_TJ + lane;          // this lane's column of the tile
+    const int stage = (int)(t % ST);
+    const int64_t j = t * TJ + lane;          // this lane's column of the tile
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
       T *tile = wtiles + (stage * NIN + k) * TSZ;
@@ -264,27 +281,52 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
         // shared operand (e.g. the vector of a vector-matrix product): one
         // element per reduction step, lane l loads step l of the tile
         const int64_t sk = d.strides[k][d.n_axes - 1];
-        const int64_t jj = t * RR_TJ + lane;
+        const int64_t jj = t * TJ + lane;
         const bool ok = jj < E;
         const T *src = ins[k] + (ok ? off[k] + jj * sk : 0);
         if constexpr (sizeof(T) == 4) cp_async4(tile + lane, src, ok);
         else cp_async8(tile + lane, src, ok);
+      } else if constexpr (VEC) {
+        // rows of the tile as 16-byte vectors: lane -> (row, vector) pairs
+        constexpr int E16 = 16 / (int)sizeof(T);
+        constexpr int VPR = TJ / E16;           // vectors per tile row
+        static_assert(VPR <= 32 && 32 % VPR == 0, "a tile row must fit one warp instruction");
+        constexpr int RPI = 32 / VPR;              // rows per instruction
+        const int v = lane % VPR;
+        if ((shared_mask >> k) & 1) {
+          // shared operand: one row, VPR lanes
+          const int64_t jj = t * TJ + v * E16;
+          const int64_t left = E - jj;
+          const int bytes = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
+          if (lane < VPR) cp_async16(tile + v * E16, ins[k] + (bytes ? off[k] + jj : 0), bytes);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32 / RPI; ++i) {
+            const int rr = i * RPI + lane / VPR;
+            const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
+            const int64_t jj = t * TJ + v * E16;
+            const int64_t left = E - jj;
+            const int bytes = (o0 + rr < n_out && left > 0)
+                                  ? (left >= E16 ? 16 : (int)left * (int)sizeof(T)) : 0;
+            cp_async16(tile + rr * RS + v * E16, ins[k] + (bytes ? base + jj : 0), bytes);
+          }
+        }
       } else if constexpr (COLS) {
         const int64_t sk = d.strides[k][d.n_axes - 1];
         for (int rr = 0; rr < 32; ++rr) {
-          const int64_t jj = t * RR_TJ + rr;       // reduction step of this tile row
+          const int64_t jj = t * TJ + rr;       // reduction step of this tile row
           const bool ok = row_ok && jj < E;
           const T *src = ins[k] + (ok ? off[k] + jj * sk : 0);
-          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * (RR_TJ + 1) + lane, src, ok);
-          else cp_async8(tile + rr * (RR_TJ + 1) + lane, src, ok);
+          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * RS + lane, src, ok);
+          else cp_async8(tile + rr * RS + lane, src, ok);
         }
       } else {
         auto copy_row = [&](int rr) {
           const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
           const bool ok = (o0 + rr < n_out) && j < E;
           const T *src = ins[k] + (ok ? base + j : 0);
-          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * (RR_TJ + 1) + lane, src, ok);
-          else cp_async8(tile + rr * (RR_TJ + 1) + lane, src, ok);
+          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * RS + lane, src, ok);
+          else cp_async8(tile + rr * RS + lane, src, ok);
         };
         if ((shared_mask >> k) & 1) {
           copy_row(0);
@@ -296,27 +338,47 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     cp_async_commit();
   };
   T acc = (row_ok && d.c0) ? static_cast<const T *>(d.c0)[o] : T(0);
-  for (int64_t t = 0; t < RR_STAGES - 1; ++t) {
+  for (int64_t t = 0; t < ST - 1; ++t) {
     if (t < ntiles) issue(t); else cp_async_commit();
   }
   for (int64_t t = 0; t < ntiles; ++t) {
-    if (t + RR_STAGES - 1 < ntiles) issue(t + RR_STAGES - 1); else cp_async_commit();
-    cp_async_wait<RR_STAGES - 1>();              // tile t has landed (this lane's copies)
+    if (t + ST - 1 < ntiles) issue(t + ST - 1); else cp_async_commit();
+    cp_async_wait<ST - 1>();              // tile t has landed (this lane's copies)
     __syncwarp();                                // ... and every lane's
-    const int stage = (int)(t % RR_STAGES);
-    const int jmax = (E - t * RR_TJ) < RR_TJ ? (int)(E - t * RR_TJ) : RR_TJ;
+    const int stage = (int)(t % ST);
+    const int jmax = (E - t * TJ) < TJ ? (int)(E - t * TJ) : TJ;
     // element c of this lane's chain: row layout tile[lane][c], column layout tile[c][lane]
     const T *row[NIN];
     int cstep[NIN];
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
       const bool sh = (shared_mask >> k) & 1;
-      row[k] = wtiles + (stage * NIN + k) * TSZ + (sh ? 0 : (COLS ? lane : lane * (RR_TJ + 1)));
-      cstep[k] = (COLS && !sh) ? RR_TJ + 1 : 1;
+      row[k] = wtiles + (stage * NIN + k) * TSZ + (sh ? 0 : (COLS ? lane : lane * RS));
+      cstep[k] = (COLS && !sh) ? RS : 1;
     }
-    if (jmax == RR_TJ) {
+    if (VEC && jmax == TJ) {
+      constexpr int E16 = 16 / (int)sizeof(T);
+#pragma unroll 2
+      for (int c4 = 0; c4 < TJ; c4 += E16) {
+        T v[NIN][E16];
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) {
+          const uint4 q = *reinterpret_cast<const uint4 *>(row[k] + c4);
+          const T *e = reinterpret_cast<const T *>(&q);
+#pragma unroll
+          for (int i = 0; i < E16; ++i) v[k][i] = e[i];
+        }
+#pragma unroll
+        for (int i = 0; i < E16; ++i) {
+          T p = v[0][i];
+#pragma unroll
+          for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, v[k][i]);
+          acc = add_rn<T>(p, acc);
+        }
+      }
+    } else if (jmax == TJ) {
 #pragma unroll 8
-      for (int c = 0; c < RR_TJ; ++c) {
+      for (int c = 0; c < TJ; ++c) {
         T p = row[0][c * cstep[0]];
 #pragma unroll
         for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * cstep[k]]);
@@ -352,9 +414,19 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   if (!rows && !cols) return false;
   if (d.extents[ax] < 64 || n_out < 32) return false;
   if (!rows && d.extents[inner] < 32) return false;   // warps would straddle short rows
-  const int64_t blocks = (n_out + 32 * RR_WARPS - 1) / (32 * RR_WARPS);
+  // 16-byte staging: rows mode, every per-row operand 16-byte aligned with
+  // its row strides in whole vectors (any reduction extent: tails are
+  // zero-filled copies)
+  bool vec = rows;
+  for (int k = 0; k < d.n_in && vec; ++k) {
+    vec = ((uintptr_t)d.ins[k] % 16) == 0;
+    for (int a = 0; a < d.n_par && vec; ++a)
+      vec = d.extents[a] == 1 || (d.strides[k][a] * (int64_t)sizeof(T)) % 16 == 0;
+  }
+  const int nw = RR_WARPS, st = RR_STAGES, tj = RR_TJ;
+  const int64_t blocks = (n_out + 32 * nw - 1) / (32 * nw);
   if (blocks > 0x7fffffffLL) return false;
-  const size_t smem = (size_t)RR_WARPS * RR_STAGES * d.n_in * 32 * (RR_TJ + 1) * sizeof(T);
+  const size_t smem = (size_t)nw * st * d.n_in * 32 * rr_stride<T>(vec, tj) * sizeof(T);
   if (smem > 200 * 1024) return false;
   uint32_t shared_mask = 0;
   for (int k = 0; k < d.n_in; ++k) {
@@ -365,9 +437,11 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   auto go = [&](auto kern) {
     // once per (kernel, device), at the largest staging this path allows
     set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
-    kern<<<(unsigned)blocks, 32 * RR_WARPS, smem, s>>>(d, n_out, shared_mask);
+    kern<<<(unsigned)blocks, 32 * nw, smem, s>>>(d, n_out, shared_mask);
   };
-  if (rows) {
+  if (rows && vec) {
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true>); else go(rowreduce_kernel<T, 2, false, true>);
+  } else if (rows) {
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, false>); else go(rowreduce_kernel<T, 2, false>);
   } else {
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, true>); else go(rowreduce_kernel<T, 2, true>);
