@@ -126,8 +126,9 @@ BGX_API int bgx_generic_tree(const bgx_generic_desc *d, void *workspace, int64_t
  *                    SIMT; f32/f64 -> BGX_MODE_EXACT.
  *   BGX_MODE_EXACT   f32/f64 CUDA-core tiles, products and sums separately
  *                    rounded in increasing k: bit-identical to the reference.
- *   BGX_MODE_FFMA    f32 CUDA-core tiles with fused multiply-add (rel. err
- *                    <= 1e-5 vs the reference, faster).
+ *   BGX_MODE_FFMA    f32/f64 CUDA-core tiles with fused multiply-add (rel.
+ *                    err <= 1e-5 vs the reference, faster); 16-bit inputs as
+ *                    BGX_MODE_AUTO.
  *   BGX_MODE_TC      tcgen05/TMEM/TMA tensor-core path (bf16/f16 inputs, f32
  *                    accumulate); BGX_ERR_UNSUPPORTED if not TMA-legal.
  *   BGX_MODE_SIMT    CUDA-core path for any dtype (f32 accumulate for 16-bit).

@@ -27,10 +27,9 @@ int select_kind(const bgx_contract_desc &d) {
       if (half_in) return KIND_SIMT16;  // exact products in f32 (see gemm_simt.cu)
       return KIND_EXACT;
     case BGX_MODE_FFMA:
-      if (d.in_dtype != BGX_F32) {
-        set_error("bgx_contract: FFMA mode needs f32 inputs");
-        return BGX_ERR_UNSUPPORTED;
-      }
+      // tolerance mode: fused multiply-add for f32 and f64; 16-bit inputs
+      // take the auto path (tensor cores when legal: products exact in f32)
+      if (half_in) return tc_legal(d, nullptr) ? KIND_TC : KIND_SIMT16;
       return KIND_FFMA;
     case BGX_MODE_TC: {
       const char *why = nullptr;

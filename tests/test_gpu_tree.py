@@ -78,3 +78,56 @@ def test_tree_faster_than_exact_chain(dev):
         torch.cuda.synchronize()
         t[mode] = s.elapsed_time(e)
     assert t["ffma"] * 20 < t["exact"], t
+
+
+@pytest.mark.parametrize("dt,mode", [(torch.float32, "ffma"), (torch.bfloat16, "auto"),
+                                     (torch.float16, "auto"), (torch.float64, "ffma")])
+def test_tolerance_paths_fuzz(dev, dt, mode):
+    """Random 1-3 input bodies on strided views, at extents that reach the
+    tree / dense-elementwise / 16-bit matrix-vector planner rules, against
+    float64 einsum of the same values (relative Frobenius error <= 1e-5 for
+    f32/f64, <= 1e-2 for 16-bit; c0 included)."""
+    import random
+    r = random.Random(4242)
+    nr = np.random.default_rng(4242)
+    from paper_2503_04771_b200 import einsum as E
+    letters = ["i", "j", "k"]
+    done = 0
+    while done < 40:
+        ins = [tuple(r.sample(letters, r.randint(1, 3))) for _ in range(r.randint(1, 3))]
+        used = sorted({x for t in ins for x in t})
+        out = tuple(r.sample(used, r.randint(0, min(2, len(used)))))
+        text = ",".join("(" + ",".join(t) + ")" for t in ins) + "->(" + ",".join(out) + ")"
+        try:
+            spec = E.parse_einsum(text)
+        except E.EinsumError:
+            continue
+        if len(spec.inputs) == 1 and set(spec.inputs[0]) == set(spec.output):
+            continue                                   # passthrough: permute path
+        ext = {a: r.choice([1, 3, 64, 200, 1500]) for a in spec.axes}
+        if np.prod([ext[a] for a in spec.axes]) > 3e8:
+            continue
+        xs = []
+        for t in spec.inputs:
+            shape = tuple(ext[x] for x in t)
+            kind = r.choice(["plain", "transpose", "slice"])
+            if kind == "transpose" and len(shape) >= 2:
+                base = torch.from_numpy(nr.standard_normal(shape[::-1])).to(dev).to(dt)
+                x = base.permute(*reversed(range(len(shape))))
+            elif kind == "slice":
+                base = torch.from_numpy(nr.standard_normal(tuple(s + 2 for s in shape))).to(dev).to(dt)
+                x = base[tuple(slice(1, 1 + s) for s in shape)]
+            else:
+                x = torch.from_numpy(nr.standard_normal(shape)).to(dev).to(dt)
+            xs.append(x)
+        c0 = torch.from_numpy(nr.standard_normal(tuple(ext[a] for a in spec.output))).to(dev).to(dt)
+        got = contract(spec, *xs, c0=c0, mode=mode).double().cpu().numpy()
+        letters_of = {a: chr(97 + n) for n, a in enumerate(spec.axes)}
+        eq = ",".join("".join(letters_of[a] for a in t) for t in spec.inputs) + "->" + \
+            "".join(letters_of[a] for a in spec.output)
+        want = np.einsum(eq, *[x.double().cpu().numpy() for x in xs]) + c0.double().cpu().numpy()
+        tol = 1e-5 if dt in (torch.float32, torch.float64) else 1e-2
+        num = np.linalg.norm(np.atleast_1d(got - want))
+        den = np.linalg.norm(np.atleast_1d(want))
+        assert num <= tol * max(den, 1e-30), (text, ext, num / den)
+        done += 1
