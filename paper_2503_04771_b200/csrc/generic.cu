@@ -271,6 +271,25 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
   }
   const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
   const int64_t ntiles = (E + TJ - 1) / TJ;
+  // VEC staging: the source of each (row group i, vector) this lane copies
+  constexpr int VE16 = 16 / (int)sizeof(T);
+  constexpr int VRPI = VEC ? 32 / (TJ / VE16) : 1;
+  constexpr int VG = VEC ? 32 / VRPI : 1;            // row groups per tile
+  const T *vsrc[NIN][VG];
+  bool vrow_ok[VG];
+  if constexpr (VEC) {
+    const int v = lane % (TJ / VE16);
+#pragma unroll
+    for (int i = 0; i < VG; ++i) {
+      const int rr = i * VRPI + lane / (TJ / VE16);
+      vrow_ok[i] = o0 + rr < n_out;
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) {
+        const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
+        vsrc[k][i] = ins[k] + base + v * VE16;
+      }
+    }
+  }
   auto issue = [&](int64_t t) {
     const int stage = (int)(t % ST);
     const int64_t j = t * TJ + lane;          // this lane's column of the tile
@@ -300,15 +319,17 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
           const int bytes = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
           if (lane < VPR) cp_async16(tile + v * E16, ins[k] + (bytes ? off[k] + jj : 0), bytes);
         } else {
+          // per-lane source pointers precomputed once (vsrc); a full tile is
+          // one pointer add + one cp.async per row group
+          const bool full = (t + 1) * TJ <= E;
+          const int64_t jj = t * TJ + v * E16;
+          const int64_t left = E - jj;
+          const int tail = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
 #pragma unroll
           for (int i = 0; i < 32 / RPI; ++i) {
             const int rr = i * RPI + lane / VPR;
-            const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
-            const int64_t jj = t * TJ + v * E16;
-            const int64_t left = E - jj;
-            const int bytes = (o0 + rr < n_out && left > 0)
-                                  ? (left >= E16 ? 16 : (int)left * (int)sizeof(T)) : 0;
-            cp_async16(tile + rr * RS + v * E16, ins[k] + (bytes ? base + jj : 0), bytes);
+            const int bytes = !vrow_ok[i] ? 0 : (full ? 16 : tail);
+            cp_async16(tile + rr * RS + v * E16, bytes ? vsrc[k][i] + t * TJ : ins[k], bytes);
           }
         }
       } else if constexpr (COLS) {
@@ -423,7 +444,11 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     for (int a = 0; a < d.n_par && vec; ++a)
       vec = d.extents[a] == 1 || (d.strides[k][a] * (int64_t)sizeof(T)) % 16 == 0;
   }
-  const int nw = RR_WARPS, st = RR_STAGES, tj = RR_TJ;
+  // fewer outputs than 4 warps per SM: one-warp blocks, so every SM streams
+  // (a warp's chains cannot be split across SMs)
+  const int sms = sm_count_current();
+  const bool thin = vec && n_out <= (int64_t)(sms > 0 ? sms : 148) * 32 * 4;
+  const int nw = thin ? 1 : RR_WARPS, st = RR_STAGES, tj = RR_TJ;
   const int64_t blocks = (n_out + 32 * nw - 1) / (32 * nw);
   if (blocks > 0x7fffffffLL) return false;
   const size_t smem = (size_t)nw * st * d.n_in * 32 * rr_stride<T>(vec, tj) * sizeof(T);
@@ -439,7 +464,10 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
     kern<<<(unsigned)blocks, 32 * nw, smem, s>>>(d, n_out, shared_mask);
   };
-  if (rows && vec) {
+  if (rows && vec && thin) {
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1>);
+    else go(rowreduce_kernel<T, 2, false, true, 1>);
+  } else if (rows && vec) {
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true>); else go(rowreduce_kernel<T, 2, false, true>);
   } else if (rows) {
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, false>); else go(rowreduce_kernel<T, 2, false>);
