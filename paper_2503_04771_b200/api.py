@@ -35,14 +35,15 @@ def output_shape(spec: EinsumSpec, operands) -> tuple:
 def contract(spec, *operands: torch.Tensor, out: torch.Tensor | None = None,
              c0: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
              mode: str = "auto", schedule=None,
-             chain_order: str = "left", devices=None) -> torch.Tensor:
+             chain_order: str = "auto", devices=None) -> torch.Tensor:
     """Evaluate an einsum spec such as ``"(i,k),(k,j)->(i,j)"`` on CUDA tensors.
 
     ``c0``: initial output (the reference's output operand; None = zeros).
     ``out``: optional preallocated result (may alias nothing else).
     ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt' (include/bgx.h).
     ``schedule``: optional ``Schedule`` / dict / ``"tile_n=512,cta_group=2"``.
-    ``chain_order``: 'left' or 'optimal' pairwise order for 3+ inputs.
+    ``chain_order``: 'auto' (left to right unless >4x the optimal cost),
+    'left' or 'optimal' pairwise order for 3+ inputs (16-bit / tolerance modes).
     ``devices``: list of CUDA devices — M-shard the contraction over them from
     this one process (``shard.contract_devices``)."""
     if devices is not None and len(devices) > 1:

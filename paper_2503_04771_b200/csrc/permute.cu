@@ -178,6 +178,28 @@ copy_rows_vec_kernel(const uint4 *__restrict__ in, uint4 *__restrict__ out, int6
   }
 }
 
+// Contiguous rows SHORTER than a block's worth of vectors (a permutation
+// that keeps a short inner dim in place, e.g. (c,a,b)->(a,c,b) with b = 64):
+// the flat (row, vector) index space is spread over all threads, 32-bit
+// index arithmetic.
+__global__ void __launch_bounds__(256)
+copy_short_rows_vec_kernel(const uint4 *__restrict__ in, uint4 *__restrict__ out, uint32_t nvec,
+                           uint32_t total, BatchDims bd) {
+  for (uint32_t g = blockIdx.x * 256u + threadIdx.x; g < total; g += gridDim.x * 256u) {
+    uint32_t r = g / nvec;
+    const uint32_t x = g - r * nvec;
+    int64_t in_off = x, out_off = x;
+    for (int d = bd.n - 1; d >= 0; --d) {
+      const uint32_t e = (uint32_t)bd.extent[d];
+      const uint32_t q = r / e, i = r - q * e;
+      r = q;
+      in_off += (int64_t)i * bd.in_stride[d];
+      out_off += (int64_t)i * bd.out_stride[d];
+    }
+    __stcs(out + out_off, __ldcs(in + in_off));
+  }
+}
+
 struct Dim {
   int64_t extent, in_stride, out_stride;
 };
@@ -218,6 +240,15 @@ int launch_permute(const void *in, void *out, std::vector<Dim> dims, cudaStream_
       for (int d = 0; d < bd.n; ++d) {
         bd.in_stride[d] /= vec;
         bd.out_stride[d] /= vec;
+      }
+      bool small32 = len < 256 && rows * len < 0x7fffffffLL;
+      for (int d = 0; d < bd.n && small32; ++d) small32 = bd.extent[d] < 0x7fffffffLL;
+      if (small32) {
+        const int64_t total = rows * len;
+        const int64_t g2 = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 32);
+        copy_short_rows_vec_kernel<<<(unsigned)g2, 256, 0, s>>>(
+            (const uint4 *)in, (uint4 *)out, (uint32_t)len, (uint32_t)total, bd);
+        return check_launch("permute copy (short rows)");
       }
       copy_rows_vec_kernel<<<(unsigned)grid, 256, 0, s>>>((const uint4 *)in, (uint4 *)out,
                                                          len, rows, chunk, nchunk, bd);

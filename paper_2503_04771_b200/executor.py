@@ -151,14 +151,8 @@ def permute(x: torch.Tensor, out: torch.Tensor, perm) -> torch.Tensor:
     return out
 
 
-def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
-            tree: bool = False) -> torch.Tensor:
-    """The reference loop nest on the device (bit-exact for f32/f64; bf16/f16
-    widened to f32, per-op f32 rounding, one final rounding to the storage
-    type — the tensor-core path's semantics).  ``tree=True`` (tolerance
-    mode, bodies with a reduction): block-wide tree reductions instead of one
-    sequential chain per output (``bgx_generic_tree``, not bit-exact)."""
-    lib = _lib.load()
+def _generic_desc(spec: EinsumSpec, inputs, c0, out):
+    """bgx_generic_desc of one generic op (c0: contiguous or None)."""
     if out.dtype not in TORCH_TO_BGX:
         raise NotImplementedError(f"bgx_generic: unsupported dtype {out.dtype}")
     if len(inputs) > _lib.MAX_OPERANDS or len(spec.axes) > _lib.MAX_AXES:
@@ -175,24 +169,61 @@ def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
         d.ins[k] = t.data_ptr()
         for dim, name in enumerate(tup):
             d.strides[k][spec.axes.index(name)] = t.stride(dim)
-    assert out.is_contiguous()
-    if c0 is not None and not c0.is_contiguous():
-        c0 = permute(c0, torch.empty(c0.shape, dtype=c0.dtype, device=c0.device),
-                     list(range(c0.dim())))
     d.c0 = c0.data_ptr() if c0 is not None else None   # NULL: zero initial output
     d.out = out.data_ptr()
+    return d
+
+
+def _launch_generic(lib, d, tree: bool, out):
+    """bgx_generic, or bgx_generic_tree with a workspace from the allocator."""
     with _on_device(out.device):
-        if tree and len(spec.axes) > len(spec.output):
+        if tree:
             ws_bytes = _lib._i64(0)
             _lib.check(lib.bgx_generic_tree_plan(d, ws_bytes), "bgx_generic_tree_plan")
             ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device=out.device)
             _lib.check(lib.bgx_generic_tree(d, ws.data_ptr(), ws_bytes.value, _stream_ptr(out)),
                        "bgx_generic_tree")
             _log("generic-tree")
-            return out
-        _lib.check(lib.bgx_generic(d, _stream_ptr(out)), "bgx_generic")
-    _log("generic")
+        else:
+            _lib.check(lib.bgx_generic(d, _stream_ptr(out)), "bgx_generic")
+            _log("generic")
     return out
+
+
+def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
+            tree: bool = False) -> torch.Tensor:
+    """The reference loop nest on the device (bit-exact for f32/f64; bf16/f16
+    widened to f32, per-op f32 rounding, one final rounding to the storage
+    type — the tensor-core path's semantics).  ``tree=True`` (tolerance
+    mode, bodies with a reduction): block-wide tree reductions instead of one
+    sequential chain per output (``bgx_generic_tree``, not bit-exact)."""
+    lib = _lib.load()
+    assert out.is_contiguous()
+    if c0 is not None and not c0.is_contiguous():
+        c0 = permute(c0, torch.empty(c0.shape, dtype=c0.dtype, device=c0.device),
+                     list(range(c0.dim())))
+    d = _generic_desc(spec, inputs, c0, out)
+    return _launch_generic(lib, d, tree and len(spec.axes) > len(spec.output), out)
+
+
+def _fast_generic(spec, inputs, c0, out, tree: bool):
+    """Pre-built descriptor for a repeated generic signature: later calls
+    patch the pointers and launch (the planning, extents and Python
+    descriptor build — tens of microseconds — are skipped)."""
+    if not out.is_contiguous() or (c0 is not None and not c0.is_contiguous()):
+        return None
+    lib = _lib.load()
+    d = _generic_desc(spec, inputs, c0, out)
+    tree = tree and len(spec.axes) > len(spec.output)
+    n = len(inputs)
+
+    def run(xs, o, c):
+        for k in range(n):
+            d.ins[k] = xs[k].data_ptr()
+        d.c0 = c.data_ptr() if c is not None else None
+        d.out = o.data_ptr()
+        _launch_generic(lib, d, tree, o)
+    return run
 
 
 def contract_raw(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0=None,
@@ -316,6 +347,7 @@ def _launch(lib, d, kind, splits, ws_bytes, out) -> int:
 
 PAD_MIN_FLOP = 1 << 28
 TREE_16BIT_POINTS = 1024
+PREREDUCE_16BIT_BLOWUP = 64
 
 
 def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0,
@@ -524,8 +556,70 @@ def _fast_permute(x, out, perm):
     return run
 
 
+def _spec_of(inputs, output) -> EinsumSpec:
+    """EinsumSpec for index tuples (axis order of einsum.py:81: output
+    indices, then input-only ones in first-appearance order)."""
+    seen = list(dict.fromkeys(a for t in inputs for a in t))
+    axes = tuple(output) + tuple(a for a in seen if a not in output)
+    return EinsumSpec(tuple(tuple(t) for t in inputs), tuple(output), axes)
+
+
+def _private_axes(spec: EinsumSpec) -> dict:
+    """Input k -> its reduction axes that no other operand carries."""
+    res = {}
+    for k, tup in enumerate(spec.inputs):
+        others = set(spec.output)
+        for j, t2 in enumerate(spec.inputs):
+            if j != k:
+                others.update(t2)
+        priv = [a for a in tup if a not in others]
+        if priv:
+            res[k] = priv
+    return res
+
+
+def _tolerance(mode: str, dt) -> bool:
+    """Paths free to reorder sums: FFMA mode, and 16-bit storage in auto mode
+    (no reference arithmetic exists for it)."""
+    return mode == "ffma" or (mode == "auto" and dt in (torch.bfloat16, torch.float16))
+
+
+def _prereduce(spec, inputs, mode):
+    """Tolerance paths: sum each input over the reduction axes only it
+    carries before it meets the others — sum_{d,b,c} x[d,a] y[d,b,c] =
+    sum_d x[d,a] (sum_{b,c} y[d,b,c]) — so no kernel walks the product space
+    of unrelated axes.  Returns the reduced (spec, inputs) or None."""
+    priv = _private_axes(spec)
+    if len(spec.inputs) < 2 or not priv:
+        return None
+    if inputs[0].dtype in (torch.bfloat16, torch.float16):
+        # 16-bit: the reduced operand is stored at 16 bits (one more rounding
+        # of an intermediate), so only where the product space dwarfs the
+        # operands (>= PREREDUCE_16BIT_BLOWUP x) — there the direct walk is
+        # the pathological part
+        ext = extents_of(spec, [t.shape for t in inputs])
+        pts = 1
+        for e in ext.values():
+            pts *= e
+        if pts < PREREDUCE_16BIT_BLOWUP * sum(t.numel() for t in inputs):
+            return None
+    new_tups, new_ins = [], []
+    for k, (tup, x) in enumerate(zip(spec.inputs, inputs)):
+        if k not in priv:
+            new_tups.append(tup)
+            new_ins.append(x)
+            continue
+        keep = tuple(a for a in tup if a not in priv[k])
+        sub = _spec_of([tup], keep)
+        y = torch.empty([x.shape[tup.index(a)] for a in keep], dtype=x.dtype, device=x.device)
+        execute(sub, [x], None, y, mode=mode)
+        new_tups.append(keep)
+        new_ins.append(y)
+    return _spec_of(new_tups, spec.output), new_ins
+
+
 def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor, *,
-            mode: str = "auto", schedule=None, chain_order: str = "left"):
+            mode: str = "auto", schedule=None, chain_order: str = "auto"):
     """Run one generic op into ``out`` (fresh, contiguous-or-strided device
     tensor).  ``c0`` is the initial output (None = zeros); ignored by a
     passthrough body, exactly as in the reference (einsum.py:105-108)."""
@@ -542,6 +636,11 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     for t in inputs:
         if t.dtype != dt:
             raise TypeError("operands must share one element type")
+    if _tolerance(mode, dt) and len(inputs) >= 2:
+        red = _prereduce(spec, inputs, mode)
+        if red is not None:
+            return execute(red[0], red[1], c0, out, mode=mode, schedule=schedule,
+                           chain_order=chain_order)
     shapes = [tuple(t.shape) for t in inputs] + [tuple(out.shape)]
     strides = [tuple(t.stride()) for t in inputs] + [tuple(out.stride())]
     plan = plan_generic(spec, shapes, strides, dtype=DTYPE_NAME[dt], mode=mode,
@@ -564,7 +663,12 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
                     red_pts *= e
             tree = red_pts >= TREE_16BIT_POINTS
         if out.is_contiguous():
-            return generic(spec, inputs, c0, out, tree=tree)
+            generic(spec, inputs, c0, out, tree=tree)
+            if key is not None:
+                fast = _fast_generic(spec, inputs, c0, out, tree)
+                if fast is not None:
+                    _cache_put(_exec_cache(), key, fast)
+            return out
         tmp = torch.empty(out.shape, dtype=dt, device=out.device)
         generic(spec, inputs, c0, tmp, tree=tree)
         return permute(tmp, out, list(range(out.dim())))
@@ -580,7 +684,7 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     raise AssertionError(plan)
 
 
-def plan_for(spec: EinsumSpec, inputs, out, *, mode="auto", chain_order="left"):
+def plan_for(spec: EinsumSpec, inputs, out, *, mode="auto", chain_order="auto"):
     shapes = [tuple(t.shape) for t in inputs] + [tuple(out.shape)]
     strides = [tuple(t.stride()) for t in inputs] + [tuple(out.stride())]
     return plan_generic(spec, shapes, strides, dtype=DTYPE_NAME[out.dtype], mode=mode,

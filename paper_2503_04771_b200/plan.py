@@ -159,7 +159,7 @@ def classify_two(spec: EinsumSpec, ext: dict):
 
 
 def plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
-                 out_strides=None, chain_order: str = "left"):
+                 out_strides=None, chain_order: str = "auto"):
     """Plan one generic op.  ``shapes``/``strides``: per operand (inputs then
     output), element strides.  ``dtype``: 'f32'|'f64'|'bf16'|'f16'.
     ``mode``: 'auto' | 'exact' | 'ffma' | 'tc' | 'simt'.  Plans are pure
@@ -181,7 +181,7 @@ def _plan_cached(spec, shapes, strides, dtype, mode, out_strides, chain_order):
 
 
 def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
-                  out_strides=None, chain_order: str = "left"):
+                  out_strides=None, chain_order: str = "auto"):
     n_in = len(spec.inputs)
     ext = extents_of(spec, shapes)
     all_par = all(a in spec.output for a in spec.axes)
@@ -280,11 +280,21 @@ def _pair_out(lhs_axes, rhs_axes, keep):
     return tuple(a for a in seen if a in keep)
 
 
+CHAIN_AUTO_FACTOR = 4
+
+
 def plan_chain(spec: EinsumSpec, ext: dict, order: str = "left") -> ChainPlan:
     """Pairwise evaluation of a 3+-input contraction.  ``order='left'`` folds
     inputs left to right (the order that shards on the output's leading free
     index with no collective); ``'optimal'`` picks the cheapest binary order
-    by exhaustive search (fine for the <= 6 operands the ABI allows)."""
+    by exhaustive search (fine for the <= 6 operands the ABI allows);
+    ``'auto'`` keeps left to right unless it costs more than
+    CHAIN_AUTO_FACTOR x the optimal order (a left fold can build an outer
+    product of unrelated operands; BASELINE C5's left order is 1.6x)."""
+    if order == "auto":
+        left = plan_chain(spec, ext, "left")
+        best = plan_chain(spec, ext, "optimal")
+        return left if left.flops <= CHAIN_AUTO_FACTOR * best.flops else best
     ins = list(spec.inputs)
 
     def needed_after(pending):

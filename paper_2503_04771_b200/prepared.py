@@ -33,7 +33,7 @@ def _sig(t: torch.Tensor):
 
 class Prepared:
     def __init__(self, spec, *tensors: torch.Tensor, out=None, c0=None, out_dtype=None,
-                 mode: str = "auto", schedule=None, chain_order: str = "left",
+                 mode: str = "auto", schedule=None, chain_order: str = "auto",
                  graph: bool = False):
         self.spec = spec if isinstance(spec, EinsumSpec) else parse_einsum(spec)
         from .schedule import as_schedule_dict

@@ -585,7 +585,7 @@ def _sharded_descriptors(spec, slabs, kw):
     """One bgx_contract_desc per slab when every slab is a plain GEMM the
     planner would launch as one bgx_contract (executor.gemm_descriptor), else
     None (permutations, chains, operand copies, split-K: per-device path)."""
-    if kw.get("schedule") or kw.get("chain_order", "left") != "left" or len(spec.inputs) != 2:
+    if kw.get("schedule") or kw.get("chain_order", "auto") not in ("left", "auto") or len(spec.inputs) != 2:
         return None
     mode = kw.get("mode", "auto")
     from .plan import GemmPlan
