@@ -439,6 +439,44 @@ def ksplit_aux(dev, world, rank):
     return res
 
 
+def scaling_projection(dev, ms_full: float, steps: int = 10):
+    """Strong-scaling projection from ONE GPU: the chain step on the row slab
+    rank 0 of an N-way M-shard would own (shard.row_range).  The M-shard has
+    no collective, so N ranks on N GPUs each run exactly this slab
+    concurrently.  Each slab is timed right after the full job, both from an
+    idle GPU (0.5 s pause), so the pair sees the same power state; speedup =
+    full-job step / slab step.  The driver's own N-GPU runs measure the real
+    thing."""
+    from paper_2503_04771_b200 import contract, shard
+    res = {"method": "per-rank slab of the 32768-row job timed on one GPU, paired with the "
+                     "full job from the same idle state (no data-path collective in the "
+                     "M-shard)", "headline_ms": ms_full}
+    A, B, C = make_inputs(I_, dev, 0)
+    O = torch.empty((I_, L_), dtype=torch.bfloat16, device=dev)
+
+    def timed(a, o, n_steps):
+        for _ in range(2):
+            contract(SPEC, a, B, C, out=o)
+        torch.cuda.synchronize()
+        time.sleep(0.5)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(n_steps):
+            contract(SPEC, a, B, C, out=o)
+        s1.record()
+        torch.cuda.synchronize()
+        return s0.elapsed_time(s1) / n_steps
+
+    for n in (2, 4, 8):
+        lo, hi = shard.row_range(I_, n, 0)
+        full = timed(A, O, 5)
+        ms = timed(A[lo:hi], O[lo:hi], steps)
+        res[f"n{n}"] = {"rows_per_rank": hi - lo, "slab_ms": ms, "full_ms_paired": full,
+                        "projected_speedup": full / ms,
+                        "projected_efficiency": full / ms / n}
+    return res
+
+
 def chain_optimal_order(dev):
     """Time-to-solution of the chain with the planner's min-flop order
     A @ (B @ C) (5.50 TFLOP executed instead of 8.80): the headline keeps the
@@ -822,6 +860,10 @@ def main():
         opt = chain_optimal_order(dev)
         opt["speedup_vs_left_to_right_time"] = ms / opt["ms"]
         aux["c5_chain_min_flop_order"] = opt
+        try:
+            aux["strong_scaling_projection"] = scaling_projection(dev, ms)
+        except Exception as e:  # noqa: BLE001
+            aux["strong_scaling_projection"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     done.set()
     line["aux"] = aux
     if rank == 0:

@@ -1198,7 +1198,13 @@ void choose_tile(const bgx_contract_desc &d, int sms, int &cg, int &bn) {
     const int64_t tail = tiles % slots;
     if (sp == 1 && tiles >= slots && tail > 0 && tail * 2 <= slots && k_blocks >= 128)
       eff_waves = (double)(tiles / slots) + 0.55;
-    const double cost = eff_waves * (double)(128 * c.bn) / c.eff;
+    // the 512-wide tile's single accumulator drains the MMA pipe at every
+    // tile boundary: with few tiles per pair (<= 6 waves) that costs more
+    // than its operand economy buys (rows x 8192 x 8192, round 2: 4096 rows
+    // 352.8 -> 340.8 us, 6144 rows 546.7 -> 530.6 us with 256-wide tiles;
+    // 8192 rows and up keep 512, profiles/r02_slab_tiles.txt)
+    const double eff = (c.bn == 512 && waves <= 6) ? 0.97 : c.eff;
+    const double cost = eff_waves * (double)(128 * c.bn) / eff;
     // single 512-column accumulator: its drain is amortised only over long K
     // and several waves (4096^3 measured faster with 256-wide tiles; 8192^3,
     // 7 waves, 5 % faster with 512: profiles/r01_tile512_8192.txt)

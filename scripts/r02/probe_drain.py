@@ -12,6 +12,7 @@ sys.path.insert(0, ".")
 from paper_2503_04771_b200 import _lib  # noqa: E402
 
 SHAPES = {"c3": (64, 1024, 1024, 1024), "c4": (1, 4096, 4096, 4096),
+          "r8192": (1, 8192, 8192, 8192), "r16384": (1, 16384, 8192, 8192), "r4096": (1, 4096, 8192, 8192),
           "chain": (1, 32768, 8192, 8192), "k2048": (16, 2048, 2048, 2048)}
 
 
@@ -63,6 +64,12 @@ def run(shape, variants):
 
 
 VARS = {
+    "rows": [("auto", {}), ("t512 r-8", {"tile_n": 512, "cta_group": 2, "raster": -8}),
+             ("t512 r-4", {"tile_n": 512, "cta_group": 2, "raster": -4}),
+             ("t512 r-16", {"tile_n": 512, "cta_group": 2, "raster": -16}),
+             ("t512 r8", {"tile_n": 512, "cta_group": 2, "raster": 8}),
+             ("t256", {"tile_n": 256, "cta_group": 2}),
+             ("t256 r-8", {"tile_n": 256, "cta_group": 2, "raster": -8})],
     "pf": [("auto", {}), ("auto pf4", {"pf": 4}), ("auto pf8", {"pf": 8}),
            ("auto pf16", {"pf": 16}), ("auto pf32", {"pf": 32}), ("auto again", {})],
     "cn2f": [("t256 quads dyn", {"tile_n": 256, "cta_group": 2, "cluster_n": 2, "debug": 128}),
