@@ -1,4 +1,9 @@
-"""Small invocation of every kernel class (for compute-sanitizer memcheck)."""
+"""Small invocation of every kernel class (for compute-sanitizer memcheck).
+
+compute-sanitizer is refused on the GPU pool (profiles/r02_sanitizer.txt);
+tests/test_gpu_guard_zones.py is the in-repo substitute: the same kernel
+classes with NaN-filled guard zones around every operand and a sentinel
+pattern around every output."""
 import os
 import sys
 
@@ -40,5 +45,20 @@ try:
     fir_gpu.run_kernel(mod, "vadd", interp.LaunchConfig((2, 1, 1), (4, 1, 1)), bufs)
 except ImportError as e:
     print("bridgegen not importable, skipping FIR kernel:", e)
+# round 2 kernels
+contract("(i,j),(i,j)->(i,j)", r(300, 136), r(300, 136))                       # dense_ew (vector)
+contract("(i,j),(i,j)->(i,j)", r(301, 137), r(301, 137))                       # dense_ew tail
+contract("(i,j)->(i)", r(700, 4096))                                           # rowreduce VEC thin
+contract("(i,j)->(i)", r(20000, 96))                                           # rowreduce VEC 4-warp
+contract("(i,j)->()", r(3000, 700), mode="ffma")                               # tree contig + finish
+contract("(i,j)->(i)", r(3000, 700), mode="ffma")                              # tree contig warp
+contract("(i,j)->(j)", r(3000, 700), mode="ffma")                              # tree column
+contract("(i,j)->(j)", r(3000, 702, dt=torch.bfloat16))                        # tree column2 (16-bit)
+contract("(k),(k,j)->(j)", r(3000, dt=torch.bfloat16), r(3000, 702, dt=torch.bfloat16))
+contract("(i,j,k)->(j)", r(40, 37, 300), mode="ffma")                          # tree general
+contract("(c,a,b)->(a,c,b)", r(70, 90, 64))                                    # short-row copy
+contract("(i)->(i)", r(1 << 20))                                               # chunked row copy
+contract("(i,k),(k,j)->(i,j)", r(1000, 320, dt=torch.bfloat16), r(320, 272, dt=torch.bfloat16),
+         devices=[0, 0])                                                       # bgx_contract_sharded
 torch.cuda.synchronize()
 print("sanitize smoke done")
