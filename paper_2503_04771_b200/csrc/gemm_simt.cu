@@ -467,6 +467,127 @@ __global__ void __launch_bounds__(256, 2) simt_f32_cp_kernel(const Params p) {
     }
 }
 
+// ---- f32, latency-bound sizes, row-major operands: cp.async ring ------------------
+// The small-problem kernel above spends as many instructions on its generic
+// strided, bounds-checked register staging as on the arithmetic; with one warp
+// per scheduler (the problem has too few outputs for more) those instructions
+// are the kernel time.  Here A (K-major) and B (N-major) tiles go global ->
+// shared with one or two 16-byte cp.async per thread per stage (zero fill at
+// the edges), SM_STAGES KT-deep stages in flight, and A fragments are read
+// four k at a time.  Each output still accumulates fl(fl(a*b) + acc) in
+// increasing k from c0 and the k loop stops at K exactly: EXACT mode stays
+// bit-identical to the reference.
+constexpr int SM_KT = 32, SM_STAGES = 4, SM_APAD = 4;
+
+template <bool FUSED, int TM, int TN>
+__global__ void __launch_bounds__(128) simt_f32_small_cp_kernel(const Params p) {
+  constexpr int NT = 128;
+  constexpr int TX = 32 / TN;              // threads along N: BN = 32
+  constexpr int BN = 32, BM = (NT / TX) * TM;
+  __shared__ __align__(16) float As[SM_STAGES][BM][SM_KT + SM_APAD];   // [s][m][k]
+  __shared__ __align__(16) float Bs[SM_STAGES][SM_KT][BN];             // [s][k][n]
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  int64_t t = blockIdx.x;
+  const int64_t tn = t % p.tiles_n;
+  t /= p.tiles_n;
+  const int64_t tm = t % p.tiles_m;
+  const int64_t b = t / p.tiles_m;
+  const int64_t m0 = tm * BM, n0 = tn * BN;
+  const float *A = static_cast<const float *>(p.a) + b * p.sa[0];
+  const float *B = static_cast<const float *>(p.b) + b * p.sb[0];
+  const int64_t lda = p.sa[1], ldb = p.sb[1];
+  const int64_t ktiles = (p.K + SM_KT - 1) / SM_KT;
+  auto issue = [&](int64_t kt) {
+    const int st = (int)(kt % SM_STAGES);
+    const int64_t k0 = kt * SM_KT;
+#pragma unroll
+    for (int c = tid; c < BM * (SM_KT / 4); c += NT) {   // A: BM rows x 8 chunks
+      const int row = c / (SM_KT / 4), kq = (c % (SM_KT / 4)) * 4;
+      const int64_t m = m0 + row, k = k0 + kq;
+      int bytes = 0;
+      if (m < p.M && k < p.K) bytes = (int)((p.K - k) >= 4 ? 16 : (p.K - k) * 4);
+      cp_async16(&As[st][row][kq], bytes ? A + m * lda + k : A, bytes);
+    }
+#pragma unroll
+    for (int c = tid; c < SM_KT * (BN / 4); c += NT) {   // B: KT rows x 8 chunks
+      const int row = c / (BN / 4), nq = (c % (BN / 4)) * 4;
+      const int64_t k = k0 + row, n = n0 + nq;
+      int bytes = 0;
+      if (k < p.K && n < p.N) bytes = (int)((p.N - n) >= 4 ? 16 : (p.N - n) * 4);
+      cp_async16(&Bs[st][row][nq], bytes ? B + k * ldb + n : B, bytes);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < SM_STAGES - 1; ++s) {
+    if (s < ktiles) issue(s);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t m = m0 + ty * TM + i, n = n0 + tx * TN + j;
+      acc[i][j] = (p.c0 && m < p.M && n < p.N)
+                      ? static_cast<const float *>(p.c0)[b * p.sc[0] + m * p.sc[1] + n * p.sc[2]]
+                      : 0.f;
+    }
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(SM_STAGES - 2) : "memory");
+    __syncthreads();                         // tile kt landed; slot kt-1 is free
+    if (kt + SM_STAGES - 1 < ktiles) issue(kt + SM_STAGES - 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const int st = (int)(kt % SM_STAGES);
+    const int kmax = (p.K - kt * SM_KT) < SM_KT ? (int)(p.K - kt * SM_KT) : SM_KT;
+    auto kstep = [&](const float (&av)[TM], int kk) {
+      float bv[TN];
+      if constexpr (TN == 4) {
+        const float4 q = *reinterpret_cast<const float4 *>(&Bs[st][kk][tx * 4]);
+        bv[0] = q.x; bv[1] = q.y; bv[2] = q.z; bv[3] = q.w;
+      } else {
+        const float2 q = *reinterpret_cast<const float2 *>(&Bs[st][kk][tx * 2]);
+        bv[0] = q.x; bv[1] = q.y;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = Arith<float>::template mac<FUSED>(av[i], bv[j], acc[i][j]);
+    };
+    if (kmax == SM_KT) {
+#pragma unroll
+      for (int kk = 0; kk < SM_KT; kk += 4) {
+        float4 a4[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a4[i] = *reinterpret_cast<const float4 *>(&As[st][ty * TM + i][kk]);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float av[TM];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) av[i] = h == 0 ? a4[i].x : h == 1 ? a4[i].y : h == 2 ? a4[i].z : a4[i].w;
+          kstep(av, kk + h);
+        }
+      }
+    } else {
+      for (int kk = 0; kk < kmax; ++kk) {
+        float av[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = As[st][ty * TM + i][kk];
+        kstep(av, kk);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  float *O = static_cast<float *>(p.out) + b * p.so[0];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t m = m0 + ty * TM + i, n = n0 + tx * TN + j;
+      if (m < p.M && n < p.N) O[m * p.so[1] + n * p.so[2]] = acc[i][j];
+    }
+}
+
 template <typename In, typename Out, typename Acc, bool FUSED>
 int launch(const bgx_contract_desc &d, cudaStream_t s) {
   Params p;
@@ -479,10 +600,28 @@ int launch(const bgx_contract_desc &d, cudaStream_t s) {
   const int sms = sm_count_current();
   const int64_t outs = d.M * d.N * d.batch;
   const bool small = outs < (int64_t)sms * 64 * 64 * 2;
-  // BGX_SIMT_SMALL (A/B only): 0 = one output per thread, 1 = four chains per thread
-  static const int small_variant = getenv("BGX_SIMT_SMALL") ? atoi(getenv("BGX_SIMT_SMALL")) : 1;
+  // BGX_SIMT_SMALL (A/B only): 0 = one output per thread, 1 = four chains per thread,
+  // 2/3/4 = f32 row-major cp.async ring with 1x4 / 1x2 / 2x2 outputs per thread
+  static const int small_variant = getenv("BGX_SIMT_SMALL") ? atoi(getenv("BGX_SIMT_SMALL")) : 4;
   const int64_t tiles_16x32 = ((d.M + 15) / 16) * ((d.N + 31) / 32) * d.batch;
-  if (outs <= (int64_t)sms * 2048 && small_variant == 1 && tiles_16x32 >= sms / 2) {
+  const bool rowmajor_f32 = std::is_same<In, float>::value && std::is_same<Out, float>::value &&
+                            d.a_stride[2] == 1 && d.b_stride[2] == 1 && d.a_stride[1] % 4 == 0 &&
+                            d.b_stride[1] % 4 == 0 && (d.batch <= 1 || (d.a_stride[0] % 4 == 0 &&
+                            d.b_stride[0] % 4 == 0)) && ((uintptr_t)d.a % 16) == 0 &&
+                            ((uintptr_t)d.b % 16) == 0;
+  if (outs <= (int64_t)sms * 2048 && small_variant >= 2 && rowmajor_f32 && tiles_16x32 >= sms / 2) {
+    // latency-bound f32 row-major: cp.async ring, no register staging
+    if (small_variant == 3) {
+      p.tiles_m = (d.M + 7) / 8; p.tiles_n = (d.N + 31) / 32;
+      simt_f32_small_cp_kernel<FUSED, 1, 2><<<(unsigned)(p.tiles_m * p.tiles_n * d.batch), 128, 0, s>>>(p);
+    } else if (small_variant == 4) {
+      p.tiles_m = (d.M + 15) / 16; p.tiles_n = (d.N + 31) / 32;
+      simt_f32_small_cp_kernel<FUSED, 2, 2><<<(unsigned)tiles_16x32, 128, 0, s>>>(p);
+    } else {
+      p.tiles_m = (d.M + 15) / 16; p.tiles_n = (d.N + 31) / 32;
+      simt_f32_small_cp_kernel<FUSED, 1, 4><<<(unsigned)tiles_16x32, 128, 0, s>>>(p);
+    }
+  } else if (outs <= (int64_t)sms * 2048 && small_variant >= 1 && tiles_16x32 >= sms / 2) {
     // latency-bound sizes: the per-output k-sequential chain is the floor;
     // four independent chains per thread (1 x 4 outputs) hide the add
     // latency and amortise the shared-memory reads, 16 x 32 tiles of 128

@@ -16,7 +16,7 @@ dev = torch.device("cuda", 0)
 lib = _lib.load()
 st = torch.cuda.current_stream().cuda_stream
 for (M, N, K) in [(256, 256, 256), (128, 128, 128), (512, 512, 512), (256, 256, 4096),
-                  (64, 1024, 256), (333, 257, 129), (1024, 1024, 1024), (2048, 2048, 512)]:
+                  (64, 1024, 256), (333, 257, 129), (332, 260, 132), (100, 36, 1000), (1024, 1024, 1024), (2048, 2048, 512)]:
     rng = np.random.default_rng(M + N + K)
     ah = rng.standard_normal((M, K), dtype=np.float32)
     bh = rng.standard_normal((K, N), dtype=np.float32)

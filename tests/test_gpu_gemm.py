@@ -73,6 +73,21 @@ def test_fp32_exact_and_ffma(dev, M, N, K, beta):
     assert oracle.rel_frobenius(np32(ff), want) <= FFMA_TOL
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 256, 256), (332, 260, 132), (250, 300, 36),
+                                   (256, 256, 1000), (64, 1024, 256)])
+@pytest.mark.parametrize("beta", [False, True])
+def test_fp32_exact_small_cp_path(dev, M, N, K, beta):
+    """Latency-bound row-major f32 (the cp.async ring kernel): ragged M/N, K
+    tails shorter than a stage, c0 — bit-identical to the reference order."""
+    a, b = rnd((M, K), 11, dev), rnd((K, N), 12, dev)
+    c0 = rnd((M, N), 13, dev) if beta else None
+    ex = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="exact")
+    want = oracle.gemm_kseq(np32(a), np32(b), np32(c0) if beta else None)
+    assert np.array_equal(np32(ex), want)
+    ff = contract("(i,k),(k,j)->(i,j)", a, b, c0=c0, mode="ffma")
+    assert oracle.rel_frobenius(np32(ff), want) <= FFMA_TOL
+
+
 def test_f64_exact(dev):
     a = rnd((33, 41), 4, dev, torch.float64)
     b = rnd((41, 19), 5, dev, torch.float64)
