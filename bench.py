@@ -869,7 +869,11 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        # the line is out: a teardown stuck behind a wedged peer must not
+        # hold the job (exit 0 after a grace period)
+        threading.Timer(60.0, lambda: os._exit(0)).start()
         dist.destroy_process_group()
+        os._exit(0)
     return 0
 
 
