@@ -46,6 +46,28 @@ def contract(spec, *operands: torch.Tensor, out: torch.Tensor | None = None,
     'left' or 'optimal' pairwise order for 3+ inputs (16-bit / tolerance modes).
     ``devices``: list of CUDA devices — M-shard the contraction over them from
     this one process (``shard.contract_devices``)."""
+    fast_key = None
+    if schedule is None and devices is None:
+        # repeated signature (spec, operand layouts, mode, output): the
+        # launcher ``execute`` cached for it, without re-deriving the output
+        # shape, the extents or the executor's key
+        try:
+            fast_key = (spec, mode, chain_order, out_dtype,
+                        tuple((t.shape, t.stride(), t.dtype, t.device, t.data_ptr() % 16)
+                              for t in operands),
+                        None if c0 is None else (c0.shape, c0.stride(), c0.dtype, c0.device,
+                                                 c0.data_ptr() % 16),
+                        None if out is None else (out.shape, out.stride(), out.dtype,
+                                                  out.device, out.data_ptr() % 16))
+            hit = _fast_cache().get(fast_key)
+        except (AttributeError, TypeError):   # not tensors: the general path reports it
+            fast_key = hit = None
+        if hit is not None:
+            shape, dt, dev, launcher = hit
+            if out is None:
+                out = torch.empty(shape, dtype=dt, device=dev)
+            launcher(list(operands), out, c0)
+            return out
     if devices is not None and len(devices) > 1:
         from .shard import contract_devices
         return contract_devices(spec, *operands, devices=devices, out=out, c0=c0,
@@ -67,8 +89,24 @@ def contract(spec, *operands: torch.Tensor, out: torch.Tensor | None = None,
         # widened output (16-bit in, f32 out): only the GEMM path supports it
         return _contract_widened(spec, operands, c0, out, mode, schedule)
     extents_of(spec, [t.shape for t in operands] + [out.shape])
-    return executor.execute(spec, list(operands), c0, out, mode=mode, schedule=schedule,
-                            chain_order=chain_order)
+    res = executor.execute(spec, list(operands), c0, out, mode=mode, schedule=schedule,
+                           chain_order=chain_order)
+    if fast_key is not None and all(t.is_cuda for t in operands):
+        launcher = executor.fast_launcher(spec, list(operands), c0, out, mode, chain_order)
+        if launcher is not None:
+            executor._cache_put(_fast_cache(), fast_key,
+                                (tuple(out.shape), out.dtype, out.device, launcher))
+    return res
+
+
+_fast_tls = threading.local()
+
+
+def _fast_cache() -> dict:
+    d = getattr(_fast_tls, "d", None)
+    if d is None:
+        d = _fast_tls.d = {}
+    return d
 
 
 def _contract_widened(spec, operands, c0, out, mode, schedule):

@@ -236,4 +236,50 @@ def _run_function(module, symbol, inputs, step_limit, mode, device, schedule):
         elem_of = {id(v): env[id(v)].elem for v in rets}
         if not all(isinstance(env[id(v)].data, torch.Tensor) for v in rets):
             replay = None
+        else:
+            replay = _direct_replay(fn, plan, env, dev, mode, device, replay) or replay
     return results, steps, replay
+
+
+def _fresh_value(elem, dims, data) -> TensorValue:
+    """TensorValue for a tensor this module just allocated with the right
+    dtype and shape (skips the constructor's conversions)."""
+    v = object.__new__(TensorValue)
+    v.elem, v.dims, v.data = elem, dims, data
+    return v
+
+
+def _direct_replay(fn, plan, env, dev, mode, device, general):
+    """Replay of a one-op function whose op ran through a cached launcher
+    (``executor.fast_launcher``: a pre-built descriptor, pointers patched per
+    call): per call only the operand layout is re-checked (strides and
+    16-byte alignment — the replay key already fixed shapes, dtypes and
+    devices), the fresh result allocated and the launcher called.  Anything
+    else (several ops, a different layout) takes the general replay."""
+    if len(plan) != 1 or len(fn.returns) != 1:
+        return None
+    op, dims, dtype, sch = plan[0]
+    if sch or fn.returns[0] is not op.results[0]:
+        return None
+    pos = {id(a): i for i, a in enumerate(fn.arguments)}
+    if not all(id(x) in pos for x in op.operands):
+        return None
+    idx = [pos[id(x)] for x in op.operands]
+    ts = [dev[id(x)] for x in op.operands]
+    out_t = dev[id(op.results[0])]
+    fast = executor.fast_launcher(op.spec, ts[:-1], ts[-1], out_t, mode)
+    if fast is None:
+        return None
+    sig = [(t.stride(), t.data_ptr() % 16) for t in ts]
+    elem = env[id(op.results[0])].elem
+    n_in = len(idx) - 1
+
+    def replay(new_inputs):
+        xs = [new_inputs[i].data for i in idx]
+        for t, (st, al) in zip(xs, sig):
+            if t.stride() != st or t.data_ptr() % 16 != al:
+                return general(new_inputs)
+        o = torch.empty(dims, dtype=dtype, device=device)
+        fast(xs[:n_in], o, xs[n_in])
+        return [_fresh_value(elem, dims, o)]
+    return replay
