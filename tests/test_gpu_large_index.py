@@ -72,3 +72,20 @@ def test_gemm_output_past_2_31(dev):
     want = a[-1:].float() @ b[:, -64:].float()
     err = ((got[-1:, -64:].float() - want).norm() / want.norm()).item()
     assert err <= 1e-2
+
+
+@pytest.mark.parametrize("text,dtype,mode", [
+    ("(i,j)->()", torch.float32, "ffma"),          # tree: contiguous, full reduction
+    ("(i,j)->(i)", torch.float32, "ffma"),         # tree: contiguous rows
+    ("(i,j)->(j)", torch.float32, "ffma"),         # tree: column reduction
+    ("(i,j)->(j)", torch.bfloat16, "auto"),        # tree: 16-bit columns, two per lane
+])
+def test_tree_reductions_past_2_31(dev, text, dtype, mode):
+    x = _fill((65600, 32768), dtype, dev, 8)
+    assert x.numel() > 1 << 31
+    got = contract(text, x, mode=mode).double()
+    dims = {"(i,j)->()": (0, 1), "(i,j)->(i)": (1,), "(i,j)->(j)": (0,)}[text]
+    want = x.double().sum(dim=dims)
+    scale = want.abs().max().item() + x.shape[dims[0]] ** 0.5
+    err = (got - want).abs().max().item() / scale
+    assert err <= (2e-2 if dtype == torch.bfloat16 else 1e-4), err
