@@ -524,51 +524,80 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
         const uint32_t acc_phase = (it / C::ACC_BUFS) & 1;
         const uint32_t d_tmem = tmem_base + acc * BN;
         int kb = 0;
-        if constexpr (SPLIT_RELEASE) {
-          const int early = nkb < STAGES ? nkb : STAGES;
+        auto commit_full = [&](int which) {
+          if (elect_one()) {
+            if constexpr (CG == 1) umma_commit(&tmem_full[which]);
+            else umma_commit_mc(&tmem_full[which], pair_mask);
+          }
+          __syncwarp();
+        };
+        // resident stages [kb, kb + n): every first-half MMA, then (after
+        // `between`) every second-half MMA, releasing each stage
+        auto split_pass = [&](int kb0, int n, auto &&between) {
           const int stage0 = stage;
           const uint32_t phase0 = phase;
-          mbar_wait(&tmem_empty[0], acc_phase ^ 1);
-          tc_fence_after();
-          for (int e = 0; e < early; ++e) {          // first half, resident stages
+          for (int e = 0; e < n; ++e) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            if (elect_one()) issue(stage, e, 0, 1, d_tmem);
+            if (elect_one()) issue(stage, kb0 + e, 0, 1, d_tmem);
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          mbar_wait(&tmem_empty[1], acc_phase ^ 1);
-          tc_fence_after();
+          between();
           stage = stage0;
           phase = phase0;
-          for (int e = 0; e < early; ++e) {          // second half, same stages
+          for (int e = 0; e < n; ++e) {
             if (elect_one()) {
-              issue(stage, e, 1, 2, d_tmem);
+              issue(stage, kb0 + e, 1, 2, d_tmem);
               release(stage);
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          kb = early;
+        };
+        if constexpr (SPLIT_RELEASE) {
+          // Tile start: the first half runs over the resident stages while
+          // the epilogue still drains the previous tile's second half.  Tile
+          // end: the last resident stages issue every first-half MMA, commit
+          // the first half (tmem_full[0]), then the second halves (tmem_full[1])
+          // — the epilogue reads columns [0,256) while the tensor core is
+          // still busy on [256,512), so the single accumulator never idles it.
+          const int early = nkb < STAGES ? nkb : STAGES;
+          const int late = (nkb - early) < STAGES ? (nkb - early) : STAGES;
+          mbar_wait(&tmem_empty[0], acc_phase ^ 1);
+          tc_fence_after();
+          split_pass(0, early, [&] {
+            if (late == 0) commit_full(0);            // all of the first half issued
+            mbar_wait(&tmem_empty[1], acc_phase ^ 1);
+            tc_fence_after();
+          });
+          for (kb = early; kb < nkb - late; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one()) {
+              issue(stage, kb, 0, 2, d_tmem);
+              release(stage);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          if (late > 0) split_pass(nkb - late, late, [&] { commit_full(0); });
+          commit_full(1);
         } else {
           mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
           tc_fence_after();
-        }
-        for (; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (elect_one()) {
-            issue(stage, kb, 0, C::NSPLIT, d_tmem);
-            release(stage);
+          for (; kb < nkb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (elect_one()) {
+              issue(stage, kb, 0, C::NSPLIT, d_tmem);
+              release(stage);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          commit_full(acc);
         }
-        if (elect_one()) {
-          if constexpr (CG == 1) umma_commit(&tmem_full[acc]);
-          else umma_commit_mc(&tmem_full[acc], pair_mask);
-        }
-        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -609,6 +638,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
       named_bar_sync(2, 32 * EPI_WARPS);
       tc_fence_after();
       constexpr bool SPLIT_RELEASE = C::ACC_BUFS == 1 && C::NSPLIT == 2;
+      // SPLIT_RELEASE: tmem_full[0] signals columns [0,256), tmem_full[1]
+      // the whole tile.  Only the two-phase drain reads the first half early;
+      // every other path waits for the whole tile here.
+      auto wait_second_half = [&] {
+        if (ew == 0) mbar_wait(&tmem_full[1], acc_phase);
+        named_bar_sync(2, 32 * EPI_WARPS);
+        tc_fence_after();
+      };
+      if constexpr (SPLIT_RELEASE) {
+        const bool two_phase = !RS && sizeof(OutT) == 2 && p.tma_store && p.c0 == nullptr &&
+                               !(p.debug & 5) && !tail;
+        if (!two_phase) wait_second_half();
+      }
       auto arrive_empty = [&](int which) {
         tc_fence_before();
         __syncwarp();
@@ -751,6 +793,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           uint32_t pk2[2][PER_HALF][16];
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
+            if (half == 1) wait_second_half();
 #pragma unroll
             for (int j = 0; j < PER_HALF; ++j) {
               const int c = half * (NCHUNK / 2) + g + 2 * j;
@@ -769,6 +812,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
 #else
 #pragma unroll 1
           for (int half = 0; half < 2; ++half) {
+            if (half == 1) wait_second_half();
             uint32_t pk[PER_HALF][16];
 #pragma unroll
             for (int j = 0; j < PER_HALF; ++j) {
