@@ -70,6 +70,12 @@ template <int IN_BYTES> struct Elem {
   static constexpr int BOX_BYTES = MN_ATOM * BK * IN_BYTES;  // one MN-major box (8 / 4 KB)
 };
 constexpr int EPI_WARPS = 8;                // 2 warps per TMEM lane quadrant
+// 512-wide tiles: resident stages whose first halves are issued ahead of
+// their second halves at a tile end (the epilogue drains columns [0,256)
+// behind them); each held stage delays its refill.
+#ifndef LATE_STAGES
+#define LATE_STAGES 4
+#endif
 constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
 constexpr int SMEM_BUDGET = 227 * 1024;
 
@@ -563,7 +569,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           // — the epilogue reads columns [0,256) while the tensor core is
           // still busy on [256,512), so the single accumulator never idles it.
           const int early = nkb < STAGES ? nkb : STAGES;
-          const int late = (nkb - early) < STAGES ? (nkb - early) : STAGES;
+          const int late_max = (p.debug >> 16) & 7 ? (p.debug >> 16) & 7 : LATE_STAGES;
+          const int late_cap = late_max < STAGES ? late_max : STAGES;
+          const int late = (nkb - early) < late_cap ? (nkb - early) : late_cap;
           mbar_wait(&tmem_empty[0], acc_phase ^ 1);
           tc_fence_after();
           split_pass(0, early, [&] {

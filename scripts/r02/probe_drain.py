@@ -99,6 +99,10 @@ VARS = {
             ("t512", {"tile_n": 512, "cta_group": 2, "cluster_n": 1}),
             ("t512 cn2", {"tile_n": 512, "cta_group": 2, "cluster_n": 2}),
             ("auto", {})],
+    "late": [("t512 late1", {"tile_n": 512, "cta_group": 2, "debug": 1 << 16}),
+             ("t512 late2", {"tile_n": 512, "cta_group": 2, "debug": 2 << 16}),
+             ("t512 late3", {"tile_n": 512, "cta_group": 2, "debug": 3 << 16}),
+             ("t512 late4", {"tile_n": 512, "cta_group": 2, "debug": 4 << 16})],
     "main": [("auto", {}), ("t256", {"tile_n": 256, "cta_group": 2}),
              ("t512", {"tile_n": 512, "cta_group": 2})],
     "stage": [("t256", {"tile_n": 256, "cta_group": 2}),
