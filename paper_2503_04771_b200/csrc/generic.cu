@@ -447,7 +447,13 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   // fewer outputs than 4 warps per SM: one-warp blocks, so every SM streams
   // (a warp's chains cannot be split across SMs)
   const int sms = sm_count_current();
-  const bool thin = vec && n_out <= (int64_t)(sms > 0 ? sms : 148) * 32 * 4;
+  const bool few = n_out <= (int64_t)(sms > 0 ? sms : 148) * 32 * 4;
+  // column mode: the per-thread loop nest keeps every SM full (this
+  // kernel's staging holds one or two blocks per SM) — 1.2-4.7x faster with
+  // many outputs and for one input; two inputs over few long columns keep
+  // the staged kernel in one-warp blocks (profiles/r02_rowreduce_cols.txt)
+  if (!rows && (!few || d.n_in == 1)) return false;
+  const bool thin = (vec || !rows) && few;
   const int nw = thin ? 1 : RR_WARPS, st = RR_STAGES, tj = RR_TJ;
   const int64_t blocks = (n_out + 32 * nw - 1) / (32 * nw);
   if (blocks > 0x7fffffffLL) return false;
@@ -471,8 +477,9 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true>); else go(rowreduce_kernel<T, 2, false, true>);
   } else if (rows) {
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, false>); else go(rowreduce_kernel<T, 2, false>);
-  } else {
-    if (d.n_in == 1) go(rowreduce_kernel<T, 1, true>); else go(rowreduce_kernel<T, 2, true>);
+  } else {   // columns (few outputs: one-warp blocks over every SM)
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, true, false, 1>);
+    else go(rowreduce_kernel<T, 2, true, false, 1>);
   }
   *rc = check_launch("rowreduce_kernel");
   return true;
