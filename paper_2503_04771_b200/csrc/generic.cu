@@ -528,12 +528,32 @@ __global__ void __launch_bounds__(CH_THREADS) chain_kernel(const bgx_generic_des
       const T *x1 = NIN > 1 ? buf + (st * NIN + 1) * CH_TILE : nullptr;
       int64_t e = 0;
       if (n == CH_TILE) {
-        // unrolled: the shared loads run ahead of the dependent add chain
+        if constexpr (sizeof(T) == 4) {
+          // 16-byte shared loads: the adds are the chain, not the loads
+          const float4 *a4 = reinterpret_cast<const float4 *>(x0);
+          const float4 *b4 = reinterpret_cast<const float4 *>(NIN > 1 ? x1 : x0);
+#pragma unroll 8
+          for (int q = 0; q < CH_TILE / 4; ++q) {
+            float4 v = a4[q];
+            if constexpr (NIN > 1) {
+              const float4 w = b4[q];
+              v.x = mul_rn<T>(v.x, w.x); v.y = mul_rn<T>(v.y, w.y);
+              v.z = mul_rn<T>(v.z, w.z); v.w = mul_rn<T>(v.w, w.w);
+            }
+            acc = add_rn<T>(v.x, acc);
+            acc = add_rn<T>(v.y, acc);
+            acc = add_rn<T>(v.z, acc);
+            acc = add_rn<T>(v.w, acc);
+          }
+          e = CH_TILE;
+        } else {
+          // unrolled: the shared loads run ahead of the dependent add chain
 #pragma unroll 16
-        for (; e < CH_TILE; ++e) {
-          T p = x0[e];
-          if constexpr (NIN > 1) p = mul_rn<T>(p, x1[e]);
-          acc = add_rn<T>(p, acc);
+          for (; e < CH_TILE; ++e) {
+            T p = x0[e];
+            if constexpr (NIN > 1) p = mul_rn<T>(p, x1[e]);
+            acc = add_rn<T>(p, acc);
+          }
         }
       }
       for (; e < n; ++e) {
@@ -578,6 +598,112 @@ bool try_chain(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream
   return true;
 }
 
+// ---- few outputs, long reductions, any operand layout ---------------------
+// One block per output element.  Each output is still ONE dependent chain of
+// adds in the reference's point order, but the per-point products
+// p = ((x1*x2)*x3)... (per-op rounding; which thread forms a product does not
+// change its bits) are formed by warps 1..7 into a shared-memory tile, each
+// thread a contiguous run of points walked with an odometer, while thread 0
+// folds the previous tile: the fold runs at the add latency whatever the
+// operand strides (broadcast operands, transposed walks, 3+ inputs).
+// points per producer thread (16 f32 / 8 f64) and per stage (3584 / 1792)
+template <typename T> constexpr int cg_per() { return sizeof(T) == 4 ? 16 : 8; }
+template <typename T> constexpr int cg_tile() { return (CH_THREADS - 32) * cg_per<T>(); }
+
+template <typename T>
+__global__ void __launch_bounds__(CH_THREADS) chain_general_kernel(const bgx_generic_desc d,
+                                                                   int64_t red) {
+  constexpr int CG_PER = cg_per<T>(), CG_TILE = cg_tile<T>();
+  __shared__ __align__(16) T buf[2][CG_TILE];
+  const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+  const int n_in = d.n_in, n_par = d.n_par, n_axes = d.n_axes;
+  // this block's output element and its operand base offsets
+  int64_t base[BGX_MAX_OPERANDS];
+  for (int k = 0; k < BGX_MAX_OPERANDS; ++k) base[k] = 0;
+  {
+    int64_t rem = blockIdx.x;
+    for (int a = n_par - 1; a >= 0; --a) {
+      const int64_t i = rem % d.extents[a];
+      rem /= d.extents[a];
+      for (int k = 0; k < n_in; ++k) base[k] += i * d.strides[k][a];
+    }
+  }
+  const int64_t ntiles = (red + CG_TILE - 1) / CG_TILE;
+  auto produce = [&](int64_t t) {
+    if (threadIdx.x < 32) return;                  // warp 0 folds
+    const int64_t e0 = t * CG_TILE + (int64_t)(threadIdx.x - 32) * CG_PER;
+    if (e0 >= red) return;
+    int64_t idx[BGX_MAX_AXES], off[BGX_MAX_OPERANDS];
+    for (int k = 0; k < n_in; ++k) off[k] = base[k];
+    int64_t rem = e0;
+    for (int a = n_axes - 1; a >= n_par; --a) {
+      idx[a] = rem % d.extents[a];
+      rem /= d.extents[a];
+      for (int k = 0; k < n_in; ++k) off[k] += idx[a] * d.strides[k][a];
+    }
+    T *dst = buf[t & 1] + (threadIdx.x - 32) * CG_PER;
+    const int n = red - e0 < CG_PER ? (int)(red - e0) : CG_PER;
+    for (int j = 0; j < n; ++j) {
+      T p = ins[0][off[0]];
+      for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k]]);
+      dst[j] = p;
+      for (int a = n_axes - 1; a >= n_par; --a) {     // odometer, innermost fastest
+        for (int k = 0; k < n_in; ++k) off[k] += d.strides[k][a];
+        if (++idx[a] < d.extents[a]) break;
+        for (int k = 0; k < n_in; ++k) off[k] -= d.extents[a] * d.strides[k][a];
+        idx[a] = 0;
+      }
+    }
+  };
+  T acc = d.c0 ? static_cast<const T *>(d.c0)[blockIdx.x] : T(0);
+  produce(0);
+  __syncthreads();
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) produce(t + 1);
+    if (threadIdx.x == 0) {
+      const T *x = buf[t & 1];
+      const int64_t n = red - t * CG_TILE < CG_TILE ? red - t * CG_TILE : CG_TILE;
+      int64_t e = 0;
+      if (n == CG_TILE) {
+        if constexpr (sizeof(T) == 4) {
+          // 16-byte shared loads: the adds are the chain, not the loads
+          const float4 *x4 = reinterpret_cast<const float4 *>(x);
+#pragma unroll 8
+          for (int q = 0; q < CG_TILE / 4; ++q) {
+            const float4 v = x4[q];
+            acc = add_rn<T>(v.x, acc);
+            acc = add_rn<T>(v.y, acc);
+            acc = add_rn<T>(v.z, acc);
+            acc = add_rn<T>(v.w, acc);
+          }
+          e = CG_TILE;
+        } else {
+#pragma unroll 16
+          for (; e < CG_TILE; ++e) acc = add_rn<T>(x[e], acc);
+        }
+      }
+      for (; e < n; ++e) acc = add_rn<T>(x[e], acc);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) static_cast<T *>(d.out)[blockIdx.x] = acc;
+}
+
+// Few outputs (<= 2 per SM) over long reductions (>= 2 tiles each): the
+// one-thread-per-output loop nest would leave almost every SM idle and wait a
+// memory round trip every few points.
+template <typename T>
+bool try_chain_general(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s,
+                       int *rc) {
+  const int sms = sm_count_current();
+  if (n_out < 1 || n_out > 2 * (int64_t)(sms > 0 ? sms : 148) || red < 2 * cg_tile<T>() ||
+      d.n_in < 1 || d.n_axes <= d.n_par)
+    return false;
+  chain_general_kernel<T><<<(unsigned)n_out, CH_THREADS, 0, s>>>(d, red);
+  *rc = check_launch("chain_general_kernel");
+  return true;
+}
+
 template <typename S, typename T>
 int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
   const int sms = sm_count_current();
@@ -600,6 +726,7 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
     static const bool no_rr = getenv("BGX_NO_ROWREDUCE") != nullptr;
     if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
     if (!no_rr && try_chain<T>(d, n_out, red, s, &rc)) return rc;
+    if (!no_rr && try_chain_general<T>(d, n_out, red, s, &rc)) return rc;
   }
   if (dense && d.n_in >= 2 && d.n_in <= 3 && red == 1) {
     bool aligned = ((uintptr_t)d.out % 16 == 0) && ((uintptr_t)d.c0 % 16 == 0);

@@ -211,3 +211,27 @@ def test_generic_fuzz_strided_views(dev):
             want = np.asarray(oracle.generic(list(spec.inputs), spec.output, host, c0))
         assert np.array_equal(np.asarray(got).view(np.uint32), want.view(np.uint32)), (text, ext)
         done += 1
+
+
+@pytest.mark.parametrize("text,ext,dtype", [
+    ("(a),(b,c,d)->()", dict(a=4, b=8, c=64, d=64), np.float32),          # broadcast operand
+    ("(d,a),(d,b,c)->(a)", dict(a=8, d=64, b=32, c=32), np.float32),     # few outputs, 2 inputs
+    ("(b,c,d),(b,c),(d)->()", dict(b=64, c=64, d=8), np.float32),        # 3 inputs, rank 0
+    ("(c,a,b),(b,c)->(a)", dict(a=3, b=512, c=40), np.float64),          # f64, transposed walk
+    ("(i,j)->(j)", dict(i=20000, j=5), np.float32),                      # strided columns
+])
+def test_few_outputs_long_reductions_bit_exact(dev, text, ext, dtype):
+    """Block-per-output chains (chain_general_kernel): the products are formed
+    by other warps in any order, the adds stay one chain in the reference's
+    point order — bit-identical to the oracle, with and without c0."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(3)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(dtype) for t in s.inputs]
+    for with_c0 in (False, True):
+        init = (rng.standard_normal([ext[a] for a in s.output]).astype(dtype) if with_c0
+                else np.zeros([ext[a] for a in s.output], dtype))
+        want = oracle.generic(s.inputs, s.output, ins, init)
+        got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                       c0=torch.from_numpy(init).to(dev) if with_c0 else None).cpu().numpy()
+        assert np.array_equal(got.reshape(-1).view(np.uint8), want.reshape(-1).view(np.uint8)), \
+            (text, with_c0)
