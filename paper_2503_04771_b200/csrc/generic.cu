@@ -41,11 +41,21 @@ template <typename S, typename T> __device__ __forceinline__ S st_as(T v) {
 template <> __device__ __forceinline__ float st_as<float, float>(float v) { return v; }
 template <> __device__ __forceinline__ double st_as<double, double>(double v) { return v; }
 
+// Thread -> output mapping when the parallel axes are walked in another
+// order than the output's (launch_generic: the innermost walked axis is the
+// one the streamed operands are contiguous along, so warp loads coalesce;
+// the output, written once, takes the strided side): row-major strides of
+// the output for each walked axis.
+struct OutMap {
+  int64_t stride[BGX_MAX_AXES];
+};
+
 // DENSE: every input is laid out exactly like the (row-major) output over the
 // parallel axes and there is no reduction — the offsets are the output index.
-template <typename S, typename T, int NIN, bool DENSE>
+// PERM: the parallel axes of `d` are in walk order; om maps them to the output.
+template <typename S, typename T, int NIN, bool DENSE, bool PERM = false>
 __global__ void __launch_bounds__(128)
-generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
+generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points, const OutMap om) {
   const int n_in = NIN > 0 ? NIN : d.n_in;
   const int n_par = d.n_par, n_axes = d.n_axes, n_red = n_axes - n_par;
   const bool passthrough = (n_in == 1 && n_red == 0);
@@ -55,6 +65,7 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
     int64_t off[BGX_MAX_OPERANDS];
 #pragma unroll
     for (int k = 0; k < BGX_MAX_OPERANDS; ++k) off[k] = DENSE ? o : 0;
+    int64_t oo = PERM ? 0 : o;   // this output's element offset
     if (!DENSE) {
       if (idx32) {   // 32-bit index arithmetic: the divisions dominate elementwise bodies
         uint32_t rem = (uint32_t)o;
@@ -63,6 +74,7 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
           const uint32_t q = rem / e, i = rem - q * e;
           rem = q;
           for (int k = 0; k < n_in; ++k) off[k] += (int64_t)i * d.strides[k][a];
+          if (PERM) oo += (int64_t)i * om.stride[a];
         }
       } else {
         int64_t rem = o;
@@ -71,25 +83,26 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
           const int64_t i = rem % e;
           rem /= e;
           for (int k = 0; k < n_in; ++k) off[k] += i * d.strides[k][a];
+          if (PERM) oo += i * om.stride[a];
         }
       }
     }
     const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
     S *out = static_cast<S *>(d.out);
     if (passthrough) {
-      out[o] = ins[0][off[0]];
+      out[oo] = ins[0][off[0]];
       continue;
     }
     // c0 == NULL: zero initial output (+0.0, as the reference's zeros array)
-    T acc = d.c0 ? ld_as<S, T>(static_cast<const S *>(d.c0) + o) : T(0);
+    T acc = d.c0 ? ld_as<S, T>(static_cast<const S *>(d.c0) + oo) : T(0);
     if (red_points == 0) {
-      out[o] = st_as<S, T>(acc);
+      out[oo] = st_as<S, T>(acc);
       continue;
     }
     if (n_red == 0) {  // elementwise body (Hadamard / outer product): one point
       T p = ld_as<S, T>(ins[0] + off[0]);
       for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ld_as<S, T>(ins[k] + off[k]));
-      out[o] = st_as<S, T>(add_rn<T>(p, acc));
+      out[oo] = st_as<S, T>(add_rn<T>(p, acc));
       continue;
     }
     // Innermost reduction axis: U points of every operand are loaded ahead
@@ -100,6 +113,21 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
     const int64_t E = d.extents[ax_in];
     int64_t sin[BGX_MAX_OPERANDS];
     for (int k = 0; k < n_in; ++k) sin[k] = d.strides[k][ax_in];
+    // operands that do not move along any reduction axis: one load per
+    // output, kept in a register (a warp-divergent re-load per point was the
+    // whole cost of bodies like (d,a,c),(c,d,b)->(b,c,d))
+    uint32_t inv = 0;
+    T fixedv[NIN > 0 ? NIN : BGX_MAX_OPERANDS];
+#pragma unroll
+    for (int k = 0; k < (NIN > 0 ? NIN : BGX_MAX_OPERANDS); ++k) {
+      if (k >= n_in) break;
+      bool moves = false;
+      for (int a = n_par; a < n_axes; ++a) moves = moves || (d.strides[k][a] != 0 && d.extents[a] > 1);
+      if (!moves) {
+        inv |= 1u << k;
+        fixedv[k] = ld_as<S, T>(ins[k] + off[k]);
+      }
+    }
     const int64_t outer = red_points / E;
     int64_t idx[BGX_MAX_AXES];
     for (int a = 0; a < n_red - 1; ++a) idx[a] = 0;
@@ -110,6 +138,11 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
 #pragma unroll
         for (int k = 0; k < (NIN > 0 ? NIN : BGX_MAX_OPERANDS); ++k) {
           if (k >= n_in) break;
+          if (inv >> k & 1) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[k][u] = fixedv[k];
+            continue;
+          }
           const S *base = ins[k] + off[k] + j * sin[k];
 #pragma unroll
           for (int u = 0; u < U; ++u) v[k][u] = ld_as<S, T>(base + u * sin[k]);
@@ -137,7 +170,7 @@ generic_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red_points) {
         idx[a] = 0;
       }
     }
-    out[o] = st_as<S, T>(acc);
+    out[oo] = st_as<S, T>(acc);
   }
 }
 
@@ -181,13 +214,80 @@ dense_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
 
 template <typename S, typename T, bool DENSE>
 void launch_generic_n(const bgx_generic_desc &d, int64_t n_out, int64_t red, unsigned blocks,
-                      cudaStream_t s) {
-  switch (d.n_in) {
-    case 1: generic_kernel<S, T, 1, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
-    case 2: generic_kernel<S, T, 2, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
-    case 3: generic_kernel<S, T, 3, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
-    default: generic_kernel<S, T, 0, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red); break;
+                      cudaStream_t s, const OutMap *om = nullptr) {
+  OutMap m{};
+  if (om) m = *om;
+  if (!DENSE && om) {
+    switch (d.n_in) {
+      case 1: generic_kernel<S, T, 1, false, true><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+      case 2: generic_kernel<S, T, 2, false, true><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+      case 3: generic_kernel<S, T, 3, false, true><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+      default: generic_kernel<S, T, 0, false, true><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+    }
+    return;
   }
+  switch (d.n_in) {
+    case 1: generic_kernel<S, T, 1, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+    case 2: generic_kernel<S, T, 2, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+    case 3: generic_kernel<S, T, 3, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+    default: generic_kernel<S, T, 0, DENSE><<<blocks, 128, 0, s>>>(d, n_out, red, m); break;
+  }
+}
+
+// Walk order of the parallel axes for the per-thread loop nest: the axis
+// along which the most streamed operands (those that move along the
+// reduction, read red_points times per output) are contiguous goes
+// innermost, so a warp's loads coalesce; operands fixed along the reduction
+// and the output (written once) count less.  Returns true and fills `w` / `om`
+// when the order differs from the output's.
+bool walk_order(const bgx_generic_desc &d, bgx_generic_desc &w, OutMap &om) {
+  const int n_par = d.n_par;
+  if (n_par < 2 || d.n_axes == n_par) return false;
+  auto score = [&](int a) {
+    if (d.extents[a] == 1) return -1.0;
+    double sc = a == n_par - 1 ? 0.25 : 0.0;       // the output's contiguous axis
+    for (int k = 0; k < d.n_in; ++k) {
+      if (d.strides[k][a] != 1) continue;
+      bool streamed = false;
+      for (int r = n_par; r < d.n_axes; ++r) streamed = streamed || (d.strides[k][r] != 0 && d.extents[r] > 1);
+      sc += streamed ? 1.0 : 0.1;
+    }
+    return sc;
+  };
+  int best = n_par - 1;
+  double bs = score(best);
+  for (int a = 0; a < n_par - 1; ++a)
+    if (score(a) > bs + 0.5) { bs = score(a); best = a; }
+  // then, just outside it, the axes the streamed operands do not move along
+  // (consecutive warps re-read the same operand lines from cache)
+  auto reuse = [&](int a) {
+    int r = 0;
+    for (int k = 0; k < d.n_in; ++k) {
+      bool streamed = false;
+      for (int x = n_par; x < d.n_axes; ++x) streamed = streamed || (d.strides[k][x] != 0 && d.extents[x] > 1);
+      if (streamed && d.strides[k][a] == 0 && d.extents[a] > 1) ++r;
+    }
+    return r;
+  };
+  int order[BGX_MAX_AXES], n = 0;
+  for (int pass = 0; pass < 2; ++pass)        // outer: moved-along axes, inner: reused ones
+    for (int a = 0; a < n_par; ++a)
+      if (a != best && (reuse(a) > 0) == (pass == 1)) order[n++] = a;
+  order[n++] = best;
+  bool same = true;
+  for (int a = 0; a < n_par; ++a) same = same && order[a] == a;
+  if (same) return false;
+  int64_t ost[BGX_MAX_AXES];
+  int64_t st = 1;
+  for (int a = n_par - 1; a >= 0; --a) { ost[a] = st; st *= d.extents[a]; }
+  w = d;
+  for (int pos = 0; pos < n_par; ++pos) {
+    const int a = order[pos];
+    w.extents[pos] = d.extents[a];
+    for (int k = 0; k < d.n_in; ++k) w.strides[k][pos] = d.strides[k][a];
+    om.stride[pos] = ost[a];
+  }
+  return true;
 }
 
 // ---- row reductions: one reduction axis, contiguous in every input ---------
@@ -740,8 +840,17 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
       return check_launch("dense_ew_kernel");
     }
   }
-  if (dense) launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);
-  else launch_generic_n<S, T, false>(d, n_out, red, (unsigned)blocks, s);
+  if (dense) {
+    launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);
+  } else {
+    static const bool no_walk = getenv("BGX_NO_WALK_ORDER") != nullptr;   // A/B only
+    bgx_generic_desc w;
+    OutMap om{};
+    if (!no_walk && walk_order(d, w, om))
+      launch_generic_n<S, T, false>(w, n_out, red, (unsigned)blocks, s, &om);
+    else
+      launch_generic_n<S, T, false>(d, n_out, red, (unsigned)blocks, s);
+  }
   return check_launch("generic_kernel");
 }
 

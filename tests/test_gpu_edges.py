@@ -235,3 +235,23 @@ def test_few_outputs_long_reductions_bit_exact(dev, text, ext, dtype):
                        c0=torch.from_numpy(init).to(dev) if with_c0 else None).cpu().numpy()
         assert np.array_equal(got.reshape(-1).view(np.uint8), want.reshape(-1).view(np.uint8)), \
             (text, with_c0)
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(d,a,c),(c,d,b)->(b,c,d)", dict(b=33, c=40, d=17, a=9)),     # walk c innermost
+    ("(d,b,a),(c,d,b)->(a,b,d)", dict(a=21, b=40, d=13, c=7)),     # walk b innermost
+    ("(i,k),(j,k)->(j,i)", dict(i=37, j=45, k=5)),
+])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_generic_walk_order_bit_exact(dev, text, ext, dtype):
+    """The per-thread loop nest walks the parallel axes with the streamed
+    operands' contiguous axis innermost (not the output's): outputs land at
+    their own offsets, each still one chain in the reference's order."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(5)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(dtype) for t in s.inputs]
+    init = rng.standard_normal([ext[a] for a in s.output]).astype(dtype)
+    want = oracle.generic(s.inputs, s.output, ins, init)
+    got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                   c0=torch.from_numpy(init).to(dev), mode="exact").cpu().numpy()
+    assert np.array_equal(got.reshape(-1).view(np.uint8), want.reshape(-1).view(np.uint8))
