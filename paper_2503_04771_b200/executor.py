@@ -202,8 +202,56 @@ def generic(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     if c0 is not None and not c0.is_contiguous():
         c0 = permute(c0, torch.empty(c0.shape, dtype=c0.dtype, device=c0.device),
                      list(range(c0.dim())))
+    spec, inputs = _materialize_transposed(spec, inputs, out)
     d = _generic_desc(spec, inputs, c0, out)
     return _launch_generic(lib, d, tree and len(spec.axes) > len(spec.output), out)
+
+
+TRANSPOSE_MIN_ELEMS = 1 << 20
+
+
+def _transposed_inputs(spec: EinsumSpec, inputs, out) -> bool:
+    """True when ``generic`` would materialise a transposed input (then the
+    launch is not cached as a plain pointer patch)."""
+    if len(spec.axes) != len(spec.output) or not spec.output or out.numel() < TRANSPOSE_MIN_ELEMS:
+        return False
+    last = spec.output[-1]
+    return any(_is_transposed(t, tup, last, out) for t, tup in zip(inputs, spec.inputs))
+
+
+def _is_transposed(t, tup, last, out) -> bool:
+    """A large input (>= 1/4 of the output's elements; small ones stay in
+    cache) that carries the output's contiguous axis at a non-unit stride."""
+    return (last in tup and t.stride(tup.index(last)) != 1 and t.shape[tup.index(last)] > 1
+            and 4 * t.numel() >= out.numel())
+
+
+def _materialize_transposed(spec: EinsumSpec, inputs, out):
+    """Bodies with no reduction (elementwise over the output, read once):
+    an input walked across its rows — it carries the output's contiguous
+    axis at a non-unit stride — is first copied into the output's axis order
+    by the tiled transpose (bytes moved, bit-exact), so the loop nest reads
+    every operand coalesced; one extra pass over that operand instead of a
+    warp-divergent load per element (profiles/r02_exact_chains.txt)."""
+    if len(spec.axes) != len(spec.output) or not spec.output or out.numel() < TRANSPOSE_MIN_ELEMS:
+        return spec, inputs
+    last = spec.output[-1]
+    new_tups, new_ins, changed = [], [], False
+    for t, tup in zip(inputs, spec.inputs):
+        if _is_transposed(t, tup, last, out):
+            order = tuple(a for a in spec.output if a in tup)
+            perm = [tup.index(a) for a in order]
+            y = torch.empty([t.shape[i] for i in perm], dtype=t.dtype, device=t.device)
+            permute(t, y, perm)
+            new_tups.append(order)
+            new_ins.append(y)
+            changed = True
+        else:
+            new_tups.append(tup)
+            new_ins.append(t)
+    if not changed:
+        return spec, inputs
+    return _spec_of(new_tups, spec.output), new_ins
 
 
 def _fast_generic(spec, inputs, c0, out, tree: bool):
@@ -681,7 +729,7 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
             tree = red_pts >= TREE_16BIT_POINTS
         if out.is_contiguous():
             generic(spec, inputs, c0, out, tree=tree)
-            if key is not None:
+            if key is not None and not _transposed_inputs(spec, inputs, out):
                 fast = _fast_generic(spec, inputs, c0, out, tree)
                 if fast is not None:
                     _cache_put(_exec_cache(), key, fast)

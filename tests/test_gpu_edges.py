@@ -255,3 +255,23 @@ def test_generic_walk_order_bit_exact(dev, text, ext, dtype):
     got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
                    c0=torch.from_numpy(init).to(dev), mode="exact").cpu().numpy()
     assert np.array_equal(got.reshape(-1).view(np.uint8), want.reshape(-1).view(np.uint8))
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(a,b,c),(b)->(c,b,a)", dict(a=128, b=64, c=130)),      # transposed input materialised first
+    ("(a,b),(b,a)->(b,a)", dict(a=1030, b=1024)),
+])
+def test_elementwise_transposed_operand_bit_exact(dev, text, ext):
+    """No-reduction bodies over >= 2^20 outputs copy a row-walked input into
+    the output's axis order first (bytes moved): still the reference's
+    fl(fl(x*y) + c0) per element, signed zeros included."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(9)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(np.float32) for t in s.inputs]
+    ins[0].reshape(-1)[::7] = -0.0
+    for init in (np.zeros([ext[a] for a in s.output], np.float32),
+                 rng.standard_normal([ext[a] for a in s.output]).astype(np.float32)):
+        want = oracle.generic(s.inputs, s.output, ins, init)
+        got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                       c0=torch.from_numpy(init).to(dev)).cpu().numpy()
+        assert np.array_equal(got.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
