@@ -227,19 +227,14 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
             _prod(ext[a] for a in m) == 1 and _prod(ext[a] for a in n) == 1:
         # a full dot product: one sequential chain (the chain kernel's case)
         return GenericPlan("dot product (one chain)")
-    if ref_types and mode in ("auto", "exact") and len(k) == 1 and (
+    if ref_types and mode in ("auto", "exact") and k and (
             _prod(ext[a] for a in m) == 1 or _prod(ext[a] for a in n) == 1):
-        # matrix-vector / batched row dots: one sequential chain per output
-        # along a contiguous axis is the row-reduction kernel's case (a GEMM
-        # tile would leave all but one row or column of every tile idle)
-        ka = k[0]
-        pairs = list(zip(spec.inputs, strides[:2]))
-        rows_ok = all(st[tup.index(ka)] == 1 for tup, st in pairs)
-        inner = spec.output[-1] if spec.output else None
-        cols_ok = inner is not None and ext[inner] >= 32 and all(
-            inner not in tup or st[tup.index(inner)] == 1 for tup, st in pairs)
-        if rows_ok or cols_ok:
-            return GenericPlan("matrix-vector (row / column reductions)")
+        # matrix-vector / batched row dots: one sequential chain per output —
+        # the row-reduction kernel's case along contiguous rows or columns,
+        # else the loop nest with its coalescing walk order (a GEMM tile
+        # would leave all but one row or column of every tile idle: a
+        # 4096-batch (1024 x 8) . (8) body took 1.04 ms on SIMT tiles)
+        return GenericPlan("matrix-vector (row / column reductions)")
     return plan_gemm(spec, ext, strides, (batch, m, n, k), out_strides)
 
 
