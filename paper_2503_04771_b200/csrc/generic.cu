@@ -318,6 +318,11 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int byt
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)),
                "l"(gmem), "r"(bytes) : "memory");
 }
+// full 16-byte copy (no zero-fill operand)
+__device__ __forceinline__ void cp_async16_full(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -355,6 +360,7 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
   if (o0 >= n_out) return;
   const int64_t o = o0 + lane;
   const bool row_ok = o < n_out;
+  const bool all_rows = o0 + 32 <= n_out;
   // this lane's row bases
   int64_t off[NIN];
 #pragma unroll
@@ -419,17 +425,24 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
           const int bytes = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
           if (lane < VPR) cp_async16(tile + v * E16, ins[k] + (bytes ? off[k] + jj : 0), bytes);
         } else {
-          // per-lane source pointers precomputed once (vsrc); a full tile is
-          // one pointer add + one cp.async per row group
+          // per-lane source pointers precomputed once (vsrc); a full tile of
+          // 32 live rows is one pointer add + one cp.async per row group
           const bool full = (t + 1) * TJ <= E;
-          const int64_t jj = t * TJ + v * E16;
-          const int64_t left = E - jj;
-          const int tail = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
+          if (full && all_rows) {
+            T *dst0 = tile + (lane / VPR) * RS + v * E16;
 #pragma unroll
-          for (int i = 0; i < 32 / RPI; ++i) {
-            const int rr = i * RPI + lane / VPR;
-            const int bytes = !vrow_ok[i] ? 0 : (full ? 16 : tail);
-            cp_async16(tile + rr * RS + v * E16, bytes ? vsrc[k][i] + t * TJ : ins[k], bytes);
+            for (int i = 0; i < 32 / RPI; ++i)
+              cp_async16_full(dst0 + i * RPI * RS, vsrc[k][i] + t * TJ);
+          } else {
+            const int64_t jj = t * TJ + v * E16;
+            const int64_t left = E - jj;
+            const int tail = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
+#pragma unroll
+            for (int i = 0; i < 32 / RPI; ++i) {
+              const int rr = i * RPI + lane / VPR;
+              const int bytes = !vrow_ok[i] ? 0 : (full ? 16 : tail);
+              cp_async16(tile + rr * RS + v * E16, bytes ? vsrc[k][i] + t * TJ : ins[k], bytes);
+            }
           }
         }
       } else if constexpr (COLS) {
@@ -554,7 +567,21 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   // the staged kernel in one-warp blocks (profiles/r02_rowreduce_cols.txt)
   if (!rows && (!few || d.n_in == 1)) return false;
   const bool thin = (vec || !rows) && few;
-  const int nw = thin ? 1 : RR_WARPS, st = RR_STAGES, tj = RR_TJ;
+  // thin rows: BGX_RR_THIN_ST (A/B only) picks the tiles in flight per warp
+  // thin rows: wide tiles (128 f32 / 64 f64 columns = one 16-byte vector per
+  // lane per row, 2-3 in flight) — the per-tile issue and wait overhead,
+  // not the bytes in flight, bounded these chains (GEMV 8192^2 123 -> 90 us,
+  // profiles/r02_rowreduce_cols.txt); BGX_RR_THIN_TJ=32/64/128 for A/B
+  static const int thin_tj_env = getenv("BGX_RR_THIN_TJ") ? atoi(getenv("BGX_RR_THIN_TJ")) : 0;
+  const int nw = thin ? 1 : RR_WARPS;
+  const bool thin_rows = thin && rows && vec;
+  int tj = RR_TJ;
+  if (thin_rows) {
+    tj = thin_tj_env ? thin_tj_env : (sizeof(T) == 4 ? 128 : 64);
+    if (tj != 32 && tj != 64 && tj != 128) tj = RR_TJ;
+    if (sizeof(T) == 8 && tj == 128) tj = 64;
+  }
+  const int st = thin_rows ? (tj == 128 ? 2 : tj == 64 ? 3 : RR_STAGES) : RR_STAGES;
   const int64_t blocks = (n_out + 32 * nw - 1) / (32 * nw);
   if (blocks > 0x7fffffffLL) return false;
   const size_t smem = (size_t)nw * st * d.n_in * 32 * rr_stride<T>(vec, tj) * sizeof(T);
@@ -570,7 +597,16 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
     kern<<<(unsigned)blocks, 32 * nw, smem, s>>>(d, n_out, shared_mask);
   };
-  if (rows && vec && thin) {
+  constexpr bool f32 = sizeof(T) == 4;
+  if (f32 && thin_rows && tj == 128) {
+    if constexpr (f32) {
+      if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, 2, 128>);
+      else go(rowreduce_kernel<T, 2, false, true, 1, 2, 128>);
+    }
+  } else if (thin_rows && tj == 64) {
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, 3, 64>);
+    else go(rowreduce_kernel<T, 2, false, true, 1, 3, 64>);
+  } else if (thin_rows) {
     if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1>);
     else go(rowreduce_kernel<T, 2, false, true, 1>);
   } else if (rows && vec) {
