@@ -568,7 +568,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
           // the first half (tmem_full[0]), then the second halves (tmem_full[1])
           // — the epilogue reads columns [0,256) while the tensor core is
           // still busy on [256,512), so the single accumulator never idles it.
-          const int early = nkb < STAGES ? nkb : STAGES;
+          const int early_max = (p.debug >> 20) & 7 ? (p.debug >> 20) & 7 : STAGES;   // A/B knob
+          const int early_cap = early_max < STAGES ? early_max : STAGES;
+          const int early = nkb < early_cap ? nkb : early_cap;
           const int late_max = (p.debug >> 16) & 7 ? (p.debug >> 16) & 7 : LATE_STAGES;
           const int late_cap = late_max < STAGES ? late_max : STAGES;
           const int late = (nkb - early) < late_cap ? (nkb - early) : late_cap;

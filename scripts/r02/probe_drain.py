@@ -99,6 +99,13 @@ VARS = {
             ("t512", {"tile_n": 512, "cta_group": 2, "cluster_n": 1}),
             ("t512 cn2", {"tile_n": 512, "cta_group": 2, "cluster_n": 2}),
             ("auto", {})],
+    "el": [("t512", {"tile_n": 512, "cta_group": 2}),
+           ("t512 e1 l1", {"tile_n": 512, "cta_group": 2, "debug": (1 << 20) | (1 << 16)}),
+           ("t512 e2 l2", {"tile_n": 512, "cta_group": 2, "debug": (2 << 20) | (2 << 16)}),
+           ("t512 e2 l4", {"tile_n": 512, "cta_group": 2, "debug": (2 << 20) | (4 << 16)}),
+           ("t512 e4 l2", {"tile_n": 512, "cta_group": 2, "debug": (4 << 20) | (2 << 16)}),
+           ("t512 e1 l4", {"tile_n": 512, "cta_group": 2, "debug": (1 << 20) | (4 << 16)}),
+           ("t256", {"tile_n": 256, "cta_group": 2})],
     "late": [("t512 late1", {"tile_n": 512, "cta_group": 2, "debug": 1 << 16}),
              ("t512 late2", {"tile_n": 512, "cta_group": 2, "debug": 2 << 16}),
              ("t512 late3", {"tile_n": 512, "cta_group": 2, "debug": 3 << 16}),
