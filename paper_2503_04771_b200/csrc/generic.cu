@@ -567,7 +567,6 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   // the staged kernel in one-warp blocks (profiles/r02_rowreduce_cols.txt)
   if (!rows && (!few || d.n_in == 1)) return false;
   const bool thin = (vec || !rows) && few;
-  // thin rows: BGX_RR_THIN_ST (A/B only) picks the tiles in flight per warp
   // thin rows: wide tiles (128 f32 / 64 f64 columns = one 16-byte vector per
   // lane per row, 2-3 in flight) — the per-tile issue and wait overhead,
   // not the bytes in flight, bounded these chains (GEMV 8192^2 123 -> 90 us,
