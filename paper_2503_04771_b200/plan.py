@@ -158,6 +158,9 @@ def classify_two(spec: EinsumSpec, ext: dict):
     return batch, m, n, k
 
 
+SMALL_16BIT_DIRECT_POINTS = 1 << 24
+
+
 def plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
                  out_strides=None, chain_order: str = "auto"):
     """Plan one generic op.  ``shapes``/``strides``: per operand (inputs then
@@ -200,6 +203,13 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
             if points > GENERIC_POINT_LIMIT:
                 why += f" ({points} points: pass mode='tf32'/'ffma' for pairwise GEMMs)"
             return GenericPlan(why)
+        if mode == "auto" and points <= SMALL_16BIT_DIRECT_POINTS:
+            # 16-bit bodies small enough to walk directly: f32 arithmetic over
+            # the whole product space and one final rounding — a pairwise
+            # chain would round each intermediate to 16 bits, which a body
+            # with cancellation turns into > 1e-2 errors
+            # (scripts/r02/prereduce_acc.py)
+            return GenericPlan("multi-operand 16-bit body, direct loop nest (f32, one rounding)")
         return plan_chain(spec, ext, order=chain_order)
     groups = classify_two(spec, ext)
     if isinstance(groups, str):

@@ -65,3 +65,21 @@ def test_generic16_through_run_function(dev):
     want = torch.from_numpy(np.asarray(oracle.generic([("i", "j")], ("i",), [x.float().cpu().numpy()],
                                                       np.zeros(17, np.float32)), np.float32))
     assert torch.equal(got.data.cpu().float(), want.bfloat16().float())
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(b,d,a),(d,c),(b,d,a)->()", dict(b=3, d=256, a=64, c=16)),   # was 1.1e-1 through a bf16 chain
+    ("(b,c),(b),(b)->()", dict(b=64, c=256)),                      # was 2.4e-2
+])
+def test_small_multi_operand_16bit_bodies_round_once(dev, text, ext):
+    """16-bit bodies with 3+ operands small enough to walk directly keep f32
+    arithmetic over the whole product space and round once (a pairwise chain
+    rounded each intermediate to bf16; with cancellation that broke 1e-2)."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(99)
+    xs = [torch.from_numpy(rng.standard_normal([ext[a] for a in t])).to(dev).bfloat16()
+          for t in s.inputs]
+    got = contract(text, *xs).double()
+    tt = ",".join("".join(t) for t in s.inputs) + "->" + "".join(s.output)
+    want = torch.einsum(tt, *[x.double() for x in xs])
+    assert ((got - want).norm() / want.norm()).item() <= 1e-2
