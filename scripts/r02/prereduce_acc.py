@@ -30,7 +30,8 @@ while n < 150:
         continue
     ext = {a: r.choice([3, 16, 64, 256, 1024]) for a in spec.axes}
     pts = int(np.prod([ext[a] for a in spec.axes]))
-    if pts > 3e8 or pts < 1e4:
+    lo_pts = float(sys.argv[2]) if len(sys.argv) > 2 else 1e4
+    if pts > 3e8 or pts < lo_pts:
         continue
     xs = [torch.from_numpy(nr.standard_normal(tuple(ext[x] for x in t))).to(dev).bfloat16()
           for t in spec.inputs]
