@@ -365,9 +365,29 @@ __global__ void __launch_bounds__(256, 2) simt_f32_cp_kernel(const Params p) {
   const float *B = static_cast<const float *>(p.b) + b * p.sb[0];
   const int64_t lda = p.sa[1], ldb = p.sb[1];
   const int64_t ktiles = (p.K + CP_BK - 1) / CP_BK;
+  // interior tiles (all 128 rows / columns live): per-thread source pointers
+  // computed once, one pointer add and one unpredicated cp.async per chunk
+  const bool interior_mn = m0 + BT <= p.M && n0 + BT <= p.N;
+  const float *a_src[2], *b_src[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int ca = tid + q * 256, cb = tid + q * 256;
+    a_src[q] = A + (m0 + ca / 4) * lda + (ca % 4) * 4;
+    b_src[q] = B + (int64_t)(cb / 32) * ldb + n0 + (cb % 32) * 4;
+  }
   auto issue = [&](int64_t kt) {
     const int st = (int)(kt % CP_STAGES);
     const int64_t k0 = kt * CP_BK;
+    if (interior_mn && k0 + CP_BK <= p.K) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = tid + q * 256;
+        cp_async16(&As[st][c / 4][(c % 4) * 4], a_src[q] + k0, 16);
+        cp_async16(&Bs[st][c / 32][(c % 32) * 4], b_src[q] + k0 * ldb, 16);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < 2; ++q) {           // A: 128 rows x 4 chunks
       const int c = tid + q * 256, row = c / 4, kq = (c % 4) * 4;
