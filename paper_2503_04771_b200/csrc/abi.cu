@@ -111,16 +111,8 @@ int bgx_clock_sample(uint64_t *out, void *stream) {
   BGX_CHECK_ARG(out != nullptr, "bgx_clock_sample: null output");
   const int sms = sm_count_current();
   if (sms <= 0) { set_error("bgx_clock_sample: no device"); return BGX_ERR_NO_DEVICE; }
-  static int configured[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
   constexpr int SMEM = 200 * 1024;   // > half an SM's shared memory: one CTA per SM
-  if (!configured[dev & 63]) {
-    RelaxedCaptureScope relaxed;
-    BGX_CUDA_TRY(cudaFuncSetAttribute(clock_sample_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-    configured[dev & 63] = 1;
-  }
+  set_max_smem_once(reinterpret_cast<const void *>(clock_sample_kernel), SMEM);
   clock_sample_kernel<<<(unsigned)sms, 32, SMEM, (cudaStream_t)stream>>>(out);
   return check_launch("clock_sample_kernel");
 }

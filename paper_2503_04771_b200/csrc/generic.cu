@@ -721,17 +721,11 @@ bool try_chain(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream
     }
   }
   const size_t smem = (size_t)2 * d.n_in * CH_TILE * sizeof(T);
-  static bool configured[2][64] = {{false}};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!configured[d.n_in == 1 ? 0 : 1][dev & 63]) {   // smem is fixed per (T, n_in)
-    RelaxedCaptureScope relaxed;
-    if (d.n_in == 1)
-      cudaFuncSetAttribute(chain_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else
-      cudaFuncSetAttribute(chain_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured[d.n_in == 1 ? 0 : 1][dev & 63] = true;
-  }
+  // smem is fixed per (T, n_in): set once per kernel and device (thread-safe)
+  if (d.n_in == 1)
+    set_max_smem_once(reinterpret_cast<const void *>(chain_kernel<T, 1>), (int)smem);
+  else
+    set_max_smem_once(reinterpret_cast<const void *>(chain_kernel<T, 2>), (int)smem);
   if (d.n_in == 1)
     chain_kernel<T, 1><<<1, CH_THREADS, smem, s>>>(d, red);
   else
