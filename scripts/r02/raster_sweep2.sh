@@ -1,0 +1,4 @@
+for v in "tile_n=256,cta_group=2,raster=-4" "tile_n=256,cta_group=2,raster=-2" "tile_n=256,cta_group=2,raster=4" "tile_n=256,cta_group=2,raster=2" "tile_n=256,cta_group=2,raster=-12" "tile_n=256,cta_group=2,raster=-6"; do
+  echo "== $v"
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_ltcfabric.sum,sm__cycles_elapsed.avg.per_second --clock-control none -k regex:tc_gemm --launch-skip 3 -c 1 python scripts/r02/one_variant.py chain $v 2>&1 | grep -E "^\s+(gpu__|dram|lts|sm__)"
+done
