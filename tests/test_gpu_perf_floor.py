@@ -65,3 +65,17 @@ def test_long_row_copy_chunks_exact(dev, n):
     assert torch.equal(contract("(i)->(i)", x), x)
     y = torch.randn(3, n, device=dev)[:, : max(1, n - 1)]     # unaligned rows: scalar path
     assert torch.equal(contract("(b,i)->(b,i)", y), y)
+
+
+@pytest.mark.parametrize("spec,shapes,ceiling_ms", [
+    ("(i,k),(k)->(i)", [(8192, 8192), (8192,)], 0.25),             # exact GEMV (row-reduction kernel), ~0.09 ms
+    ("(i,k)->(i)", [(8192, 8192)], 0.25),                           # exact row sums, ~0.08 ms
+    ("(a),(b,c,d)->()", [(4,), (64, 256, 256)], 150.0),             # block-per-output chain, ~47 ms (was ~470)
+    ("(d,a,c),(c,d,b)->(b,c,d)", [(256, 64, 64), (64, 256, 256)], 60.0),  # walk order + invariant hoist
+])
+def test_exact_generic_ceilings(dev, spec, shapes, ceiling_ms):
+    """Exact (reference-order) generic bodies: generous time ceilings on the
+    round-2 kernel paths, so a planner or kernel regression fails here."""
+    xs = [torch.randn(s, device=dev) for s in shapes]
+    ms = _ms(lambda: contract(spec, *xs), iters=3)
+    assert ms <= ceiling_ms, f"{spec}: {ms:.2f} ms > {ceiling_ms}"
