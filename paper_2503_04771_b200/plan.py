@@ -159,6 +159,10 @@ def classify_two(spec: EinsumSpec, ext: dict):
 
 
 SMALL_16BIT_DIRECT_POINTS = 1 << 24
+SMALL_BATCHED_GEMM = True      # A/B switch
+SMALL_BATCHED_MN = 1024        # output elements per batch entry (<= 32 x 32), f32/f64
+SMALL_BATCHED_MN_16BIT = 256   # 16-bit: the tensor-core tiles win from 32 x 32 up
+SMALL_BATCHED_K = 256
 
 
 def plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
@@ -215,6 +219,14 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
     if isinstance(groups, str):
         return GenericPlan(groups)
     batch, m, n, k = groups
+    if batch and k and SMALL_BATCHED_GEMM and \
+            _prod(ext[a] for a in m) * _prod(ext[a] for a in n) <= \
+            (SMALL_BATCHED_MN if ref_types else SMALL_BATCHED_MN_16BIT) and \
+            _prod(ext[a] for a in k) <= SMALL_BATCHED_K:
+        # many tiny matrices: a GEMM tile (>= 128 x 64) would be almost all
+        # padding; the loop nest (one chain per output, coalescing walk
+        # order, operands reused from cache) moves the bytes instead
+        return GenericPlan("small batched GEMM")
     if not k and (not m or not n):
         # Hadamard-type bodies (no reduction, no M x N structure): a GEMM plan
         # would be batch x 1 x 1 x 1 (round 2: a 16-bit 8192^2 Hadamard took

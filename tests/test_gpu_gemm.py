@@ -458,3 +458,20 @@ def test_tc_and_tf32_modes_pad_odd_shapes(dev):
     y = contract("(i,k),(k,j)->(i,j)", ah, bh, mode="tc")
     assert any(k.startswith("tcgen05") for k in executor.launch_log())
     assert float((y.double() - ah.double() @ bh.double()).norm() / want.norm()) <= 1e-2
+
+
+@pytest.mark.parametrize("bt,m,n,k", [(4096, 8, 8, 8), (1024, 16, 16, 16), (512, 32, 32, 32),
+                                      (2048, 4, 4, 64)])
+def test_small_batched_gemms(dev, bt, m, n, k):
+    """Many tiny matrices go to the loop nest (plan 'small batched GEMM'):
+    f32 bit-identical to the reference order, bf16 within the tolerance."""
+    a = rnd((bt, m, k), 91, dev)
+    b = rnd((bt, k, n), 92, dev)
+    got = contract("(b,i,k),(b,k,j)->(b,i,j)", a, b).cpu().numpy()
+    A, B = np32(a), np32(b)
+    for i in (0, bt // 2, bt - 1):
+        assert np.array_equal(got[i], oracle.gemm_kseq(A[i], B[i])), i
+    ah, bh = a.bfloat16(), b.bfloat16()
+    g16 = contract("(b,i,k),(b,k,j)->(b,i,j)", ah, bh).float().cpu().numpy()
+    want = np.einsum("bik,bkj->bij", np32(ah).astype(np.float64), np32(bh).astype(np.float64))
+    assert oracle.rel_frobenius(g16, want) <= BF16_TOL
