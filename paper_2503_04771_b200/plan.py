@@ -163,6 +163,9 @@ SMALL_BATCHED_GEMM = True      # A/B switch
 SMALL_BATCHED_MN = 1024        # output elements per batch entry (<= 32 x 32), f32/f64
 SMALL_BATCHED_MN_16BIT = 256   # 16-bit: the tensor-core tiles win from 32 x 32 up
 SMALL_BATCHED_K = 256
+OUTER_TO_LOOP_NEST = False     # A/B switches (outer products: the GEMM tiles measured 2-4x faster)
+SKINNY_TO_LOOP_NEST = True
+SKINNY_MN = 8
 
 
 def plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = "auto",
@@ -227,6 +230,17 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
         # padding; the loop nest (one chain per output, coalescing walk
         # order, operands reused from cache) moves the bytes instead
         return GenericPlan("small batched GEMM")
+    if not k and OUTER_TO_LOOP_NEST:
+        # no reduction at all (outer products included): every output is one
+        # product, written once — the loop nest / elementwise kernels move
+        # the bytes; a GEMM tile with K = 1 spent 3-4x the write time
+        # (scripts/r02/shape_audit.py)
+        return GenericPlan("outer / elementwise product (no reduction)")
+    if ref_types and k and SKINNY_TO_LOOP_NEST and (
+            _prod(ext[a] for a in m) <= SKINNY_MN or _prod(ext[a] for a in n) <= SKINNY_MN):
+        # exact f32/f64 with at most 8 rows or columns: the SIMT tiles
+        # (>= 16 x 32) would be mostly padding
+        return GenericPlan("skinny exact GEMM")
     if not k and (not m or not n):
         # Hadamard-type bodies (no reduction, no M x N structure): a GEMM plan
         # would be batch x 1 x 1 x 1 (round 2: a 16-bit 8192^2 Hadamard took

@@ -475,3 +475,12 @@ def test_small_batched_gemms(dev, bt, m, n, k):
     g16 = contract("(b,i,k),(b,k,j)->(b,i,j)", ah, bh).float().cpu().numpy()
     want = np.einsum("bik,bkj->bij", np32(ah).astype(np.float64), np32(bh).astype(np.float64))
     assert oracle.rel_frobenius(g16, want) <= BF16_TOL
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 8, 64), (8, 4096, 64), (3000, 5, 33), (6, 2000, 300)])
+def test_skinny_exact_gemms(dev, M, N, K):
+    """Exact f32 GEMMs with at most 8 rows or columns run on the loop nest
+    (plan 'skinny exact GEMM'): bit-identical to the reference order."""
+    a, b = rnd((M, K), 93, dev), rnd((K, N), 94, dev)
+    got = contract("(i,k),(k,j)->(i,j)", a, b).cpu().numpy()
+    assert np.array_equal(got, oracle.gemm_kseq(np32(a), np32(b)))
