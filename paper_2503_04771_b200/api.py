@@ -113,6 +113,11 @@ def _contract_widened(spec, operands, c0, out, mode, schedule):
     from .plan import GemmPlan
     plan = executor.plan_for(spec, list(operands), out, mode=mode)
     if not isinstance(plan, GemmPlan):
+        # the planner prefers another kernel for the storage dtype (small
+        # batched / skinny / matrix-vector bodies), but widened outputs exist
+        # only on the GEMM path
+        plan = executor.gemm_plan_for(spec, list(operands), out)
+    if not isinstance(plan, GemmPlan):
         raise NotImplementedError("a widened output dtype needs a 2-input contraction")
     return executor.run_gemm(plan, spec, list(operands), c0, out, mode=mode, schedule=schedule)
 

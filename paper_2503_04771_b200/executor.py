@@ -749,6 +749,22 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
     raise AssertionError(plan)
 
 
+def gemm_plan_for(spec: EinsumSpec, inputs, out):
+    """The GEMM plan of a 2-input contraction regardless of the planner's
+    preference for other kernels (widened outputs exist only on the GEMM
+    path), or None when the body has no batch/M/N/K structure."""
+    from .plan import classify_two, plan_gemm
+    if len(inputs) != 2:
+        return None
+    shapes = [tuple(t.shape) for t in inputs] + [tuple(out.shape)]
+    strides = [tuple(t.stride()) for t in inputs] + [tuple(out.stride())]
+    ext = extents_of(spec, shapes)
+    groups = classify_two(spec, ext)
+    if isinstance(groups, str):
+        return None
+    return plan_gemm(spec, ext, strides, groups)
+
+
 def plan_for(spec: EinsumSpec, inputs, out, *, mode="auto", chain_order="auto"):
     shapes = [tuple(t.shape) for t in inputs] + [tuple(out.shape)]
     strides = [tuple(t.stride()) for t in inputs] + [tuple(out.stride())]

@@ -72,7 +72,10 @@ def test_chained_generics_stay_on_device(dev):
     executor.reset_launch_log()
     [out] = I.run_function(module, "twice", [I.TensorValue(E.F32, x.shape, x) for x in (a, b, zero)])
     assert G.bits_equal(out.data, want)
-    assert executor.launch_log().count("simt-exact") == 2
+    # two device launches, no host round trip (tiny operands: the skinny
+    # exact GEMM rule may pick the loop nest instead of SIMT tiles)
+    log = executor.launch_log()
+    assert len(log) == 2 and set(log) <= {"simt-exact", "generic"}, log
 
 
 def test_modes_agree_within_tolerance(dev):
