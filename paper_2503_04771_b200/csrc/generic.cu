@@ -825,14 +825,14 @@ __global__ void __launch_bounds__(CH_THREADS) chain_general_kernel(const bgx_gen
   if (threadIdx.x == 0) static_cast<T *>(d.out)[blockIdx.x] = acc;
 }
 
-// Few outputs (<= 2 per SM) over long reductions (>= 2 tiles each): the
+// Few outputs (<= 4 per SM) over long reductions (>= 2 tiles each): the
 // one-thread-per-output loop nest would leave almost every SM idle and wait a
 // memory round trip every few points.
 template <typename T>
 bool try_chain_general(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s,
                        int *rc) {
   const int sms = sm_count_current();
-  if (n_out < 1 || n_out > 2 * (int64_t)(sms > 0 ? sms : 148) || red < 2 * cg_tile<T>() ||
+  if (n_out < 1 || n_out > 4 * (int64_t)(sms > 0 ? sms : 148) || red < 2 * cg_tile<T>() ||
       d.n_in < 1 || d.n_axes <= d.n_par)
     return false;
   chain_general_kernel<T><<<(unsigned)n_out, CH_THREADS, 0, s>>>(d, red);
