@@ -81,6 +81,80 @@ tree_partial_kernel(const bgx_generic_desc d, int64_t n_out, int64_t red, int sp
     const int64_t hi = lo + chunk < red ? lo + chunk : red;
     T acc = 0;
     const bool one_axis = n_red == 1, idx32 = red <= 0x7fffffffLL;
+    const int ax_in = d.n_par + n_red - 1;
+    if (!one_axis && d.extents[ax_in] >= TR_THREADS) {
+      // innermost reduction axis at least a block wide: decode point r once,
+      // then walk it with an odometer (one carry into the outer axes at most
+      // per step) instead of a full mixed-radix decode per point
+      const int64_t E = d.extents[ax_in];
+      int64_t r = lo + threadIdx.x;
+      if (r < hi) {
+        int64_t idx[BGX_MAX_AXES];
+        int64_t off[BGX_MAX_OPERANDS];
+#pragma unroll
+        for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+          if (k < n_in) off[k] = base[k];
+        int64_t rem = r;
+        for (int a = n_red - 1; a >= 0; --a) {
+          const int ax = d.n_par + a;
+          idx[a] = rem % d.extents[ax];
+          rem /= d.extents[ax];
+#pragma unroll
+          for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+            if (k < n_in) off[k] += idx[a] * d.strides[k][ax];
+        }
+        auto step_odometer = [&]() {
+          // advance by TR_THREADS points: inner axis, then at most one carry
+          idx[n_red - 1] += TR_THREADS;
+#pragma unroll
+          for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+            if (k < n_in) off[k] += (int64_t)TR_THREADS * d.strides[k][ax_in];
+          if (idx[n_red - 1] >= E) {
+            idx[n_red - 1] -= E;
+#pragma unroll
+            for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+              if (k < n_in) off[k] -= E * d.strides[k][ax_in];
+            for (int a = n_red - 2; a >= 0; --a) {
+              const int ax = d.n_par + a;
+#pragma unroll
+              for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+                if (k < n_in) off[k] += d.strides[k][ax];
+              if (++idx[a] < d.extents[ax]) break;
+#pragma unroll
+              for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+                if (k < n_in) off[k] -= d.extents[ax] * d.strides[k][ax];
+              idx[a] = 0;
+            }
+          }
+        };
+        // the odometer position after each step; up to GU points gathered
+        // and loaded together (independent loads in flight per thread)
+        constexpr int GU = 4;
+        while (r < hi) {
+          int64_t offs[GU][BGX_MAX_OPERANDS];
+          int nu = 0;
+          for (; nu < GU && r < hi; ++nu, r += TR_THREADS) {
+#pragma unroll
+            for (int k = 0; k < BGX_MAX_OPERANDS; ++k)
+              if (k < n_in) offs[nu][k] = off[k];
+            step_odometer();
+          }
+          T pv[GU];
+#pragma unroll
+          for (int u = 0; u < GU; ++u) {
+            if (u >= nu) break;
+            T p = ld_t<S, T>(ins[0] + offs[u][0]);
+#pragma unroll
+            for (int k = 1; k < BGX_MAX_OPERANDS; ++k)
+              if (k < n_in) p *= ld_t<S, T>(ins[k] + offs[u][k]);
+            pv[u] = p;
+          }
+#pragma unroll
+          for (int u = 0; u < GU; ++u)
+            if (u < nu) acc += pv[u];
+        }
+      }
+    } else
     for (int64_t r = lo + threadIdx.x; r < hi; r += TR_THREADS) {
       int64_t off[BGX_MAX_OPERANDS];
 #pragma unroll
