@@ -402,7 +402,9 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
       T *tile = wtiles + (stage * NIN + k) * TSZ;
-      if (COLS && ((shared_mask >> k) & 1)) {
+      if ((shared_mask >> (8 + k)) & 1) {
+        // constant along the reduction (a per-output factor): never staged
+      } else if (COLS && ((shared_mask >> k) & 1)) {
         // shared operand (e.g. the vector of a vector-matrix product): one
         // element per reduction step, lane l loads step l of the tile
         const int64_t sk = d.strides[k][d.n_axes - 1];
@@ -472,6 +474,12 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     cp_async_commit();
   };
   T acc = (row_ok && d.c0) ? static_cast<const T *>(d.c0)[o] : T(0);
+  // operands constant along the reduction (shared_mask bits 8..15): one
+  // value per lane, multiplied in at their place in the left fold
+  T invv[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k)
+    invv[k] = (((shared_mask >> (8 + k)) & 1) && row_ok) ? ins[k][off[k]] : T(0);
   for (int64_t t = 0; t < ST - 1; ++t) {
     if (t < ntiles) issue(t); else cp_async_commit();
   }
@@ -497,6 +505,11 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
         T v[NIN][E16];
 #pragma unroll
         for (int k = 0; k < NIN; ++k) {
+          if ((shared_mask >> (8 + k)) & 1) {
+#pragma unroll
+            for (int i = 0; i < E16; ++i) v[k][i] = invv[k];
+            continue;
+          }
           const uint4 q = *reinterpret_cast<const uint4 *>(row[k] + c4);
           const T *e = reinterpret_cast<const T *>(&q);
 #pragma unroll
@@ -513,16 +526,18 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     } else if (jmax == TJ) {
 #pragma unroll 8
       for (int c = 0; c < TJ; ++c) {
-        T p = row[0][c * cstep[0]];
+        T p = ((shared_mask >> 8) & 1) ? invv[0] : row[0][c * cstep[0]];
 #pragma unroll
-        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * cstep[k]]);
+        for (int k = 1; k < NIN; ++k)
+          p = mul_rn<T>(p, ((shared_mask >> (8 + k)) & 1) ? invv[k] : row[k][c * cstep[k]]);
         acc = add_rn<T>(p, acc);
       }
     } else {
       for (int c = 0; c < jmax; ++c) {
-        T p = row[0][c * cstep[0]];
+        T p = ((shared_mask >> 8) & 1) ? invv[0] : row[0][c * cstep[0]];
 #pragma unroll
-        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, row[k][c * cstep[k]]);
+        for (int k = 1; k < NIN; ++k)
+          p = mul_rn<T>(p, ((shared_mask >> (8 + k)) & 1) ? invv[k] : row[k][c * cstep[k]]);
         acc = add_rn<T>(p, acc);
       }
     }
@@ -537,14 +552,24 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2 || d.n_par < 1) return false;
   const int ax = d.n_axes - 1, inner = d.n_par - 1;
   bool rows = true, cols = true;
+  // rows mode may carry operands constant along the reduction (a per-output
+  // factor, loaded once per lane) as long as one operand streams the row
+  uint32_t inv_mask = 0;
+  bool streamed = false;
   for (int k = 0; k < d.n_in; ++k) {
-    rows = rows && d.strides[k][ax] == 1;
+    if (d.strides[k][ax] == 0 && d.extents[ax] > 1) inv_mask |= 1u << k;
+    else streamed = streamed || d.strides[k][ax] == 1;
+  }
+  if (!streamed || inv_mask == (1u << d.n_in) - 1) inv_mask = 0;
+  for (int k = 0; k < d.n_in; ++k) {
+    rows = rows && (d.strides[k][ax] == 1 || ((inv_mask >> k) & 1));
     // consecutive outputs at consecutive addresses (or the input ignores the
     // output index entirely)
     bool shared = true;
     for (int a = 0; a < d.n_par; ++a) shared = shared && (d.strides[k][a] == 0 || d.extents[a] == 1);
     cols = cols && (d.strides[k][inner] == 1 || shared);
   }
+  if (inv_mask) cols = false;
   if (!rows && !cols) return false;
   if (d.extents[ax] < 64 || n_out < 32) return false;
   if (!rows && d.extents[inner] < 32) return false;   // warps would straddle short rows
@@ -553,6 +578,7 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   // zero-filled copies)
   bool vec = rows;
   for (int k = 0; k < d.n_in && vec; ++k) {
+    if ((inv_mask >> k) & 1) continue;
     vec = ((uintptr_t)d.ins[k] % 16) == 0;
     for (int a = 0; a < d.n_par && vec; ++a)
       vec = d.extents[a] == 1 || (d.strides[k][a] * (int64_t)sizeof(T)) % 16 == 0;
@@ -594,8 +620,9 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   for (int k = 0; k < d.n_in; ++k) {
     bool shared = true;
     for (int a = 0; a < d.n_par; ++a) shared = shared && (d.strides[k][a] == 0 || d.extents[a] == 1);
-    if (shared) shared_mask |= 1u << k;
+    if (shared && !((inv_mask >> k) & 1)) shared_mask |= 1u << k;
   }
+  shared_mask |= inv_mask << 8;
   auto go = [&](auto kern) {
     // once per (kernel, device), at the largest staging this path allows
     set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);

@@ -312,3 +312,22 @@ def test_random_specs_round2_kernel_classes_bit_exact(dev):
         assert np.array_equal(np.asarray(got).view(np.uint32), want.view(np.uint32)), \
             (text, ext, n_out)
         seen += 1
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(i,k),(i)->(i)", dict(i=300, k=1000)),                     # per-row factor, thin rows
+    ("(d,a,b),(c)->(d,c,a)", dict(d=3, c=50, a=40, b=700)),      # factor indexed by another output axis
+    ("(i,k),(i)->(i)", dict(i=20000, k=130)),                    # many rows, 4-warp blocks
+])
+def test_row_reduction_with_invariant_factor_bit_exact(dev, text, ext):
+    """Row reductions where one operand is constant along the reduction (a
+    per-output factor, loaded once per lane in the staged kernel): still the
+    reference's fold and order, bit for bit."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(17)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(np.float32) for t in s.inputs]
+    init = rng.standard_normal([ext[a] for a in s.output]).astype(np.float32)
+    want = oracle.generic(s.inputs, s.output, ins, init)
+    got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                   c0=torch.from_numpy(init).to(dev)).cpu().numpy()
+    assert np.array_equal(got.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
