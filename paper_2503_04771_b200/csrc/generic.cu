@@ -547,10 +547,201 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
   if (row_ok) static_cast<T *>(d.out)[o] = acc;
 }
 
+// ---- exact column chains, 16-byte staged ----------------------------------
+// Column sums and vector-matrix products in the reference order: output
+// column i is the sequential chain over the reduction rows.  One warp owns 32
+// adjacent columns (lane = column); each 32-row x 32-column tile of every
+// per-column operand is staged with 16-byte cp.async (8 rows per instruction
+// for f32) from source pointers computed once, and the fold is fully unrolled
+// with compile-time shared-memory offsets — the general rowreduce column mode
+// spends ~4x more instructions per element on runtime addressing (ncu: 2.5
+// cycles per issued instruction, 17 % issue-busy, 1.5 TB/s).  SHM bit k:
+// operand k is shared by the 32 columns (the vector of a GEMV): one element
+// per lane per tile, read back as a broadcast.
+
+template <typename T, int NIN, int SHM, int ST, int CPW>
+__global__ void __launch_bounds__(32)
+colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
+  constexpr int E16 = 16 / (int)sizeof(T);
+  constexpr int GPR = CPW / E16;             // 16-byte groups per tile row
+  static_assert(GPR >= 1 && 32 % GPR == 0, "a tile row is whole 16-byte groups");
+  constexpr int RPI = 32 / GPR;              // tile rows per copy instruction
+  constexpr int RS = CPW + E16;              // tile row stride (elements)
+  constexpr int TSZ = 32 * RS;
+  constexpr int NPC = NIN - __builtin_popcount(SHM);   // per-column operands
+  constexpr int SSZ = NPC * TSZ + (NIN - NPC) * 32;    // one stage
+  extern __shared__ __align__(16) uint8_t cc_smem_raw[];
+  const int lane = threadIdx.x;
+  T *wst = reinterpret_cast<T *>(cc_smem_raw);
+  const int64_t o0 = (int64_t)blockIdx.x * CPW;
+  if (o0 >= n_out) return;
+  const int64_t o = o0 + lane % CPW;   // lanes >= CPW fold a duplicate chain, never stored
+  const int ax = d.n_axes - 1;
+  const int64_t E = d.extents[ax];
+  // the column group's bases (its CPW outputs are adjacent columns)
+  int64_t base[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) base[k] = 0;
+  {
+    int64_t rem = o0;
+    for (int a = d.n_par - 1; a >= 0; --a) {
+      const int64_t e = d.extents[a], i = rem % e;
+      rem /= e;
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) base[k] += i * d.strides[k][a];
+    }
+  }
+  const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+  const T *src[NIN];
+  int64_t step[NIN];   // source advance per tile
+  const int q = lane % GPR, r0 = lane / GPR;
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) {
+    const int64_t sk = d.strides[k][ax];
+    if ((SHM >> k) & 1) src[k] = ins[k] + base[k] + lane * sk;
+    else src[k] = ins[k] + base[k] + r0 * sk + q * E16;
+    step[k] = 32 * sk;
+  }
+  const int64_t ntiles = (E + 31) / 32;
+  auto issue = [&](int64_t t) {
+    T *stg = wst + (int)(t % ST) * SSZ;
+    const bool full = (t + 1) * 32 <= E;
+    int pc = 0, sc = 0;
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      const T *g = src[k] + t * step[k];
+      if ((SHM >> k) & 1) {
+        T *dst = stg + NPC * TSZ + sc * 32 + lane;
+        const bool ok = full || t * 32 + lane < E;
+        if constexpr (sizeof(T) == 4) cp_async4(dst, ok ? g : ins[k], ok);
+        else cp_async8(dst, ok ? g : ins[k], ok);
+        ++sc;
+      } else {
+        T *dst = stg + pc * TSZ + r0 * RS + q * E16;
+        const int64_t rstep = RPI * d.strides[k][ax];
+        if (full) {
+#pragma unroll
+          for (int i = 0; i < 32 / RPI; ++i) cp_async16_full(dst + i * RPI * RS, g + i * rstep);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32 / RPI; ++i) {
+            const bool ok = t * 32 + i * RPI + r0 < E;
+            cp_async16(dst + i * RPI * RS, ok ? g + i * rstep : ins[k], ok ? 16 : 0);
+          }
+        }
+        ++pc;
+      }
+    }
+    cp_async_commit();
+  };
+  T acc = d.c0 ? static_cast<const T *>(d.c0)[o] : T(0);
+  // (reading a full tile into registers and refilling its stage before the
+  // add chain, to issue in the chain's shadow, was 10-15 % slower)
+  for (int64_t t = 0; t < ST - 1; ++t) {
+    if (t < ntiles) issue(t); else cp_async_commit();
+  }
+  for (int64_t t = 0; t < ntiles; ++t) {
+    if (t + ST - 1 < ntiles) issue(t + ST - 1); else cp_async_commit();
+    cp_async_wait<ST - 1>();
+    __syncwarp();
+    const T *stg = wst + (int)(t % ST) * SSZ;
+    const T *col[NIN];
+    {
+      int pc = 0, sc = 0;
+#pragma unroll
+      for (int k = 0; k < NIN; ++k) {
+        if ((SHM >> k) & 1) col[k] = stg + NPC * TSZ + 32 * sc++;
+        else col[k] = stg + (pc++) * TSZ + lane % CPW;
+      }
+    }
+    auto elem = [&](int k, int c) { return ((SHM >> k) & 1) ? col[k][c] : col[k][c * RS]; };
+    if ((t + 1) * 32 <= E) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        T p = elem(0, c);
+#pragma unroll
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, elem(k, c));
+        acc = add_rn<T>(p, acc);
+      }
+    } else {
+      const int jmax = (int)(E - t * 32);
+      for (int c = 0; c < jmax; ++c) {
+        T p = elem(0, c);
+#pragma unroll
+        for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, elem(k, c));
+        acc = add_rn<T>(p, acc);
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  if (lane < CPW) static_cast<T *>(d.out)[o] = acc;
+}
+
+// Column chains (colchain_kernel) when every warp's 32 (or 8) outputs are
+// adjacent columns (output count and innermost output extent multiples of the
+// group) and every
+// operand either moves with the innermost output axis at unit stride, 16-byte
+// aligned rows (staged), or ignores it (warp-uniform: staged once per step).
+// Fewer than CC_MIN_OUT outputs leave too few warps to stream HBM; those keep
+// the block-per-output chain kernels.  BGX_NO_COLCHAIN=1 for A/B.
+constexpr int64_t CC_MIN_OUT = 512;
+
+template <typename T>
+bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int *rc) {
+  static const bool off = getenv("BGX_NO_COLCHAIN") != nullptr;
+  const int ax = d.n_axes - 1, inner = d.n_par - 1;
+  if (off || n_out < CC_MIN_OUT || n_out % 8 || d.extents[inner] % 8 || d.extents[ax] < 64 ||
+      n_out / 8 > 0x7fffffffLL)
+    return false;
+  int shm = 0;
+  for (int k = 0; k < d.n_in; ++k) {
+    if (d.strides[k][inner] == 0) { shm |= 1 << k; continue; }
+    if (d.strides[k][inner] != 1 || ((uintptr_t)d.ins[k] % 16) != 0 ||
+        (d.strides[k][ax] * (int64_t)sizeof(T)) % 16 != 0)
+      return false;
+    for (int a = 0; a < inner; ++a)
+      if (d.extents[a] > 1 && (d.strides[k][a] * (int64_t)sizeof(T)) % 16 != 0) return false;
+  }
+  if (shm == (1 << d.n_in) - 1) return false;
+  // one warp per block (4-warp blocks: 10-40 % slower, scripts/r02/rr_vcols_ab.sh).
+  // A warp's chains advance one tile per ~500 cycles whatever the pipeline
+  // depth, so with fewer 32-column groups than SMs the columns are split 8 per
+  // warp — 4x the warps — and the 8-column tiles keep 8 in flight
+  const int sms = sm_count_current() > 0 ? sm_count_current() : 148;
+  static const int cpw_env = getenv("BGX_CC_CPW") ? atoi(getenv("BGX_CC_CPW")) : 0;
+  int cpw = cpw_env == 8 || cpw_env == 32 ? cpw_env : (n_out / 32 >= sms ? 32 : 8);
+  if (n_out % cpw || d.extents[inner] % cpw) return false;
+  const int64_t warps = n_out / cpw;
+  const int st = warps >= 2 * sms ? 4 : 8;
+  constexpr int E16 = 16 / (int)sizeof(T);
+  const int npc = d.n_in - __builtin_popcount(shm);
+  const size_t smem = (size_t)st * (npc * 32 * (cpw + E16) + (d.n_in - npc) * 32) * sizeof(T);
+  auto go = [&](auto kern) {
+    set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
+    kern<<<(unsigned)warps, 32, smem, s>>>(d, n_out);
+  };
+  auto pick = [&](auto stc, auto cpwc) {
+    constexpr int ST = decltype(stc)::value, CPW = decltype(cpwc)::value;
+    if (d.n_in == 1) go(colchain_kernel<T, 1, 0, ST, CPW>);
+    else if (shm == 0) go(colchain_kernel<T, 2, 0, ST, CPW>);
+    else if (shm == 1) go(colchain_kernel<T, 2, 1, ST, CPW>);
+    else go(colchain_kernel<T, 2, 2, ST, CPW>);
+  };
+  using I4 = std::integral_constant<int, 4>;
+  using I8 = std::integral_constant<int, 8>;
+  using I32 = std::integral_constant<int, 32>;
+  if (cpw == 32) { if (st == 4) pick(I4{}, I32{}); else pick(I8{}, I32{}); }
+  else { if (st == 4) pick(I4{}, I8{}); else pick(I8{}, I8{}); }
+  *rc = check_launch("colchain_kernel");
+  return true;
+}
+
 template <typename T>
 bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int *rc) {
   if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2 || d.n_par < 1) return false;
   const int ax = d.n_axes - 1, inner = d.n_par - 1;
+  if (try_colchain<T>(d, n_out, s, rc)) return true;
   bool rows = true, cols = true;
   // rows mode may carry operands constant along the reduction (a per-output
   // factor, loaded once per lane) as long as one operand streams the row

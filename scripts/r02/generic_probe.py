@@ -13,11 +13,12 @@ ext = dict(a=1024, d=1024, c=64, b=64)
 if len(sys.argv) > 2:
     ext = {k: int(v) for k, v in (kv.split("=") for kv in sys.argv[2].split(","))}
 mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
+dt = getattr(torch, sys.argv[4]) if len(sys.argv) > 4 else torch.float32
 ins, out = spec.split("->")
 tups = [t.strip("()").split(",") for t in ins.split("),(")]
 otup = [x for x in out.strip("()").split(",") if x]
-xs = [torch.randn([ext[a] for a in t], device=dev) for t in tups]
-o = torch.empty([ext[a] for a in otup], device=dev)
+xs = [torch.randn([ext[a] for a in t], device=dev, dtype=dt) for t in tups]
+o = torch.empty([ext[a] for a in otup], device=dev, dtype=dt)
 for _ in range(3):
     contract(spec, *xs, out=o, mode=mode)
 torch.cuda.synchronize()
@@ -28,4 +29,4 @@ for _ in range(5):
     contract(spec, *xs, out=o, mode=mode)
 e1.record()
 torch.cuda.synchronize()
-print(spec, ext, mode, f"{e0.elapsed_time(e1) / 5 * 1e3:.1f} us", executor.launch_log()[:3])
+print(spec, ext, mode, str(dt)[6:], f"{e0.elapsed_time(e1) / 5 * 1e3:.1f} us", executor.launch_log()[:3])

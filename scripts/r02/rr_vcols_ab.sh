@@ -1,0 +1,25 @@
+# exact column chains: colchain_kernel (16-byte staged, unrolled fold) vs the
+# previous paths (BGX_NO_COLCHAIN=1), and its columns per warp (BGX_CC_CPW)
+P="python scripts/r02/generic_probe.py"
+for env in "BGX_NO_COLCHAIN=1" "BGX_X=1" "BGX_CC_CPW=32" "BGX_CC_CPW=8"; do
+  echo "== $env"
+  env $env $P "(k,i),(k)->(i)" k=8192,i=8192
+  env $env $P "(k,i),(k)->(i)" k=8192,i=8192 auto float64
+  env $env $P "(b,k,i),(b,k)->(b,i)" b=64,k=1024,i=1024
+  env $env $P "(i,k)->(k)" i=8192,k=8192
+  env $env $P "(i,k)->(k)" i=8192,k=8192 auto float64
+  env $env $P "(b,c),(b)->(c)" b=4096,c=4096
+  env $env $P "(b,c),(b)->(c)" b=128,c=262144
+  env $env $P "(b,c)->(c)" b=4096,c=4096
+  for c in 1024 2048 4096; do
+    env $env $P "(b,c)->(c)" b=$((16777216 / c)),c=$c
+    env $env $P "(b,c),(b)->(c)" b=$((16777216 / c)),c=$c
+  done
+  env $env $P "(b,c)->(c)" b=65536,c=256
+  env $env $P "(b,c)->(c)" b=65536,c=256 auto float64
+  env $env $P "(b,c),(b)->(c)" b=1048576,c=16
+  env $env $P "(b,c),(b)->(c)" b=65536,c=512
+  env $env $P "(b,c)->(c)" b=32768,c=512 auto float64
+  env $env $P "(a,b,c)->(a,c)" a=16,b=4096,c=256
+  env $env $P "(k,i),(k,i)->(i)" k=4096,i=8192
+done

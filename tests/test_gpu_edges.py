@@ -331,3 +331,39 @@ def test_row_reduction_with_invariant_factor_bit_exact(dev, text, ext):
     got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
                    c0=torch.from_numpy(init).to(dev)).cpu().numpy()
     assert np.array_equal(got.reshape(-1).view(np.uint32), want.reshape(-1).view(np.uint32))
+
+
+@pytest.mark.parametrize("text,ext,dtype", [
+    ("(k,i)->(i)", dict(k=777, i=8192), np.float32),               # 32 columns per warp, tail tile
+    ("(k,i),(k)->(i)", dict(k=1000, i=1024), np.float32),          # 8 columns per warp, shared vector
+    ("(k),(k,i)->(i)", dict(k=300, i=2048), np.float32),           # shared operand first
+    ("(k,i),(k,i)->(i)", dict(k=130, i=5120), np.float32),         # both operands per column
+    ("(b,k,i),(b,k)->(b,i)", dict(b=3, k=500, i=512), np.float64),  # operand shared within a warp only
+    ("(a,b,c)->(a,c)", dict(a=4, b=333, c=256), np.float64),
+    ("(k,i)->(i)", dict(k=64, i=520), np.float32),                 # shortest staged reduction
+])
+def test_column_chains_bit_exact(dev, text, ext, dtype):
+    """Column sums and vector-matrix products on the staged column-chain
+    kernel (16-byte copies, 8 or 32 adjacent columns per warp): every output's
+    chain runs the reference's order, bit for bit, with c0."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(23)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(dtype) for t in s.inputs]
+    init = rng.standard_normal([ext[a] for a in s.output]).astype(dtype)
+    want = np.asarray(oracle.generic(s.inputs, s.output, ins, init))
+    got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                   c0=torch.from_numpy(init).to(dev)).cpu().numpy()
+    uint = np.uint32 if dtype == np.float32 else np.uint64
+    assert np.array_equal(got.reshape(-1).view(uint), want.reshape(-1).view(uint)), text
+
+
+def test_column_chains_unaligned_view_bit_exact(dev):
+    """A column slice starting off a 16-byte boundary cannot be staged with
+    16-byte copies: the planner's other exact path takes it, same bits."""
+    rng = np.random.default_rng(29)
+    big = torch.from_numpy(rng.standard_normal((700, 4100)).astype(np.float32)).to(dev)
+    for lo in (1, 4):
+        sl = big[:, lo:lo + 4096]
+        got = contract("(k,i)->(i)", sl).cpu().numpy()
+        want = np.asarray(oracle.generic([("k", "i")], ("i",), [sl.cpu().numpy()], np.zeros(4096, np.float32)))
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), lo
