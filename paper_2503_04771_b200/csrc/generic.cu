@@ -212,6 +212,86 @@ dense_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
   }
 }
 
+// Elementwise bodies with broadcast or strided operands (outer products,
+// scalings, (c),(a,c),(b)->(c,a,b)): the output is dense, so a thread takes V
+// consecutive outputs along the innermost output axis (one 16-byte store),
+// decodes their row once, and loads each operand as one 16-byte vector (unit
+// stride, aligned), one broadcast scalar (stride 0) or V strided scalars.
+// The per-output index decode of generic_kernel (a division per axis per
+// output) was the cost: 33.5M-output outer product 229 us ~ 0.6 TB/s.
+// Same per-element arithmetic as generic_kernel: p = left fold of products,
+// out = p + c0 (or + 0).
+template <typename S, typename T, int NIN>
+__global__ void __launch_bounds__(256) bcast_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
+  constexpr int V = 16 / (int)sizeof(S);
+  const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+  const S *c0 = static_cast<const S *>(d.c0);
+  S *out = static_cast<S *>(d.out);
+  const int np = d.n_par;
+  const int64_t E = d.extents[np - 1];
+  int64_t sin[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) sin[k] = d.strides[k][np - 1];
+  const int64_t nv = n_out / V;
+  const bool idx32 = n_out <= 0x7fffffffLL;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = i * V;
+    int64_t row, j;
+    if (idx32) { row = (uint32_t)o / (uint32_t)E; j = (uint32_t)o - (uint32_t)row * (uint32_t)E; }
+    else { row = o / E; j = o - row * E; }
+    int64_t off[NIN];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) off[k] = j * sin[k];
+    if (idx32) {
+      uint32_t rem = (uint32_t)row;
+      for (int a = np - 2; a >= 0; --a) {
+        const uint32_t e = (uint32_t)d.extents[a], q = rem / e, x = rem - q * e;
+        rem = q;
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) off[k] += (int64_t)x * d.strides[k][a];
+      }
+    } else {
+      int64_t rem = row;
+      for (int a = np - 2; a >= 0; --a) {
+        const int64_t e = d.extents[a], x = rem % e;
+        rem /= e;
+#pragma unroll
+        for (int k = 0; k < NIN; ++k) off[k] += x * d.strides[k][a];
+      }
+    }
+    T v[NIN][V];
+#pragma unroll
+    for (int k = 0; k < NIN; ++k) {
+      const S *src = ins[k] + off[k];
+      if (sin[k] == 0) {
+        const T x = ld_as<S, T>(src);
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[k][e] = x;
+      } else if (sin[k] == 1 && ((uintptr_t)src & 15) == 0) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(src);
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[k][e] = ld_as<S, T>(reinterpret_cast<const S *>(&q) + e);
+      } else {
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[k][e] = ld_as<S, T>(src + e * sin[k]);
+      }
+    }
+    uint4 cq = c0 ? *reinterpret_cast<const uint4 *>(c0 + o) : make_uint4(0, 0, 0, 0);
+    uint4 r;
+    S *re = reinterpret_cast<S *>(&r);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      T p = v[0][e];
+#pragma unroll
+      for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, v[k][e]);
+      const T acc = c0 ? ld_as<S, T>(reinterpret_cast<const S *>(&cq) + e) : T(0);
+      re[e] = st_as<S, T>(add_rn<T>(p, acc));
+    }
+    __stcs(reinterpret_cast<uint4 *>(out + o), r);
+  }
+}
+
 template <typename S, typename T, bool DENSE>
 void launch_generic_n(const bgx_generic_desc &d, int64_t n_out, int64_t red, unsigned blocks,
                       cudaStream_t s, const OutMap *om = nullptr) {
@@ -1017,6 +1097,28 @@ __global__ void __launch_bounds__(CH_THREADS) chain_general_kernel(const bgx_gen
     }
     T *dst = buf[t & 1] + (threadIdx.x - 32) * CG_PER;
     const int n = red - e0 < CG_PER ? (int)(red - e0) : CG_PER;
+    const int ai = n_axes - 1;
+    if (n == CG_PER && ai >= n_par && idx[ai] + CG_PER <= d.extents[ai]) {
+      // the run stays on the innermost reduction axis: CG_PER independent
+      // loads per operand in flight (the odometer loop below waits a memory
+      // round trip per point — the producers, not the fold, bounded
+      // gathers like (a,c,b),(b,a),(b)->(b))
+      T v[CG_PER];
+      const int64_t s0 = d.strides[0][ai];
+#pragma unroll
+      for (int j = 0; j < CG_PER; ++j) v[j] = ins[0][off[0] + j * s0];
+      for (int k = 1; k < n_in; ++k) {
+        const int64_t sk = d.strides[k][ai];
+        T w[CG_PER];
+#pragma unroll
+        for (int j = 0; j < CG_PER; ++j) w[j] = ins[k][off[k] + j * sk];
+#pragma unroll
+        for (int j = 0; j < CG_PER; ++j) v[j] = mul_rn<T>(v[j], w[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < CG_PER; ++j) dst[j] = v[j];
+      return;
+    }
     for (int j = 0; j < n; ++j) {
       T p = ins[0][off[0]];
       for (int k = 1; k < n_in; ++k) p = mul_rn<T>(p, ins[k][off[k]]);
@@ -1064,8 +1166,55 @@ bool try_chain_general(const bgx_generic_desc &d, int64_t n_out, int64_t red, cu
   return true;
 }
 
+// Drop extent-1 axes and merge neighbouring axes of the same kind (parallel
+// with parallel, reduction with reduction) that every input walks as one:
+// stride[a] == extent[a+1] * stride[a+1].  The output is dense row-major over
+// the parallel axes, so merging them never changes an output address, and a
+// merged reduction axis visits the points in the same order — the reference's
+// loop nest, bit for bit.  (d,b,a)->(a) with (d,b) contiguous becomes a
+// single-axis column reduction and takes colchain_kernel; BGX_NO_COALESCE=1 for A/B.
+bgx_generic_desc coalesce_axes(const bgx_generic_desc &d) {
+  static const bool off = getenv("BGX_NO_COALESCE") != nullptr;
+  if (off) return d;
+  for (int a = 0; a < d.n_axes; ++a)
+    if (d.extents[a] == 0) return d;
+  bgx_generic_desc w = d;
+  int n = 0, n_par = 0;
+  for (int a = 0; a < d.n_axes; ++a) {
+    const bool par = a < d.n_par;
+    if (d.extents[a] == 1) continue;
+    // merge into the previous kept axis when it is the same kind and contiguous with this one
+    if (n > 0 && (par == (n - 1 < n_par))) {
+      bool ok = true;
+      for (int k = 0; k < d.n_in && ok; ++k) ok = w.strides[k][n - 1] == d.extents[a] * d.strides[k][a];
+      if (ok) {
+        w.extents[n - 1] *= d.extents[a];
+        for (int k = 0; k < d.n_in; ++k) w.strides[k][n - 1] = d.strides[k][a];
+        continue;
+      }
+    }
+    w.extents[n] = d.extents[a];
+    for (int k = 0; k < d.n_in; ++k) w.strides[k][n] = d.strides[k][a];
+    ++n;
+    if (par) ++n_par;
+  }
+  if (n == 0) return d;
+  if (n == n_par && d.n_axes > d.n_par) {
+    // every reduction axis had extent 1: keep one, so the body still adds
+    // its single point to c0 (a one-input body without reduction axes is a
+    // plain copy)
+    w.extents[n] = 1;
+    for (int k = 0; k < d.n_in; ++k) w.strides[k][n] = 0;
+    ++n;
+  }
+  w.n_axes = n;
+  w.n_par = n_par;
+  return w;
+}
+
 template <typename S, typename T>
-int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s) {
+int launch_generic(const bgx_generic_desc &d0, int64_t n_out, int64_t red, cudaStream_t s) {
+  const bgx_generic_desc d = coalesce_axes(d0);
   const int sms = sm_count_current();
   if (sms <= 0) { set_error("bgx_generic: no device"); return BGX_ERR_NO_DEVICE; }
   int64_t blocks = (n_out + 127) / 128;
@@ -1084,9 +1233,12 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
     int rc = 0;
     // BGX_NO_ROWREDUCE=1: force the per-thread loop nest (A/B timing only)
     static const bool no_rr = getenv("BGX_NO_ROWREDUCE") != nullptr;
-    if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
+    // few outputs over long reductions first: a block per output folds at the
+    // add latency, where the row / column kernels' few warps pay a tile
+    // pipeline per 32 points ((d,b,a)->(d) 256 x 16384: 127 -> 58 us)
     if (!no_rr && try_chain<T>(d, n_out, red, s, &rc)) return rc;
     if (!no_rr && try_chain_general<T>(d, n_out, red, s, &rc)) return rc;
+    if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
   }
   if (dense && d.n_in >= 2 && d.n_in <= 3 && red == 1) {
     bool aligned = ((uintptr_t)d.out % 16 == 0) && ((uintptr_t)d.c0 % 16 == 0);
@@ -1099,6 +1251,19 @@ int launch_generic(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaSt
       else dense_ew_kernel<S, T, 3><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
       return check_launch("dense_ew_kernel");
     }
+  }
+  // broadcast / strided elementwise bodies: V outputs per thread along the
+  // innermost output axis (BGX_NO_BCAST_EW=1 for A/B)
+  static const bool no_bcast = getenv("BGX_NO_BCAST_EW") != nullptr;
+  if (!no_bcast && !dense && d.n_axes == d.n_par && d.n_par >= 1 && d.n_in >= 2 && d.n_in <= 3 &&
+      red == 1 && d.extents[d.n_par - 1] % (16 / (int64_t)sizeof(S)) == 0 &&
+      (uintptr_t)d.out % 16 == 0 && (uintptr_t)d.c0 % 16 == 0) {
+    int64_t vb = (n_out / (16 / (int64_t)sizeof(S)) + 255) / 256;
+    if (vb > (int64_t)sms * 16) vb = (int64_t)sms * 16;
+    if (vb < 1) vb = 1;
+    if (d.n_in == 2) bcast_ew_kernel<S, T, 2><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+    else bcast_ew_kernel<S, T, 3><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+    return check_launch("bcast_ew_kernel");
   }
   if (dense) {
     launch_generic_n<S, T, true>(d, n_out, red, (unsigned)blocks, s);

@@ -367,3 +367,67 @@ def test_column_chains_unaligned_view_bit_exact(dev):
         got = contract("(k,i)->(i)", sl).cpu().numpy()
         want = np.asarray(oracle.generic([("k", "i")], ("i",), [sl.cpu().numpy()], np.zeros(4096, np.float32)))
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), lo
+
+
+@pytest.mark.parametrize("text,ext,dtype", [
+    ("(d,b,a)->(a)", dict(d=300, b=8, a=1024), np.float32),        # (d,b) merge: one column chain axis
+    ("(d,b,a)->(a)", dict(d=100, b=8, a=1024), np.float64),
+    ("(d,b,a)->(d)", dict(d=256, b=64, a=64), np.float32),          # (b,a) merge: row chains
+    ("(a,b,c),(c)->(a,b)", dict(a=16, b=64, c=300), np.float32),   # (a,b) parallel merge
+    ("(j,l,k)->(l,j)", dict(j=7, l=7, k=1), np.float32),           # every reduction axis unit
+    ("(a,k,b),(k)->(a,b)", dict(a=1, k=1, b=40), np.float64),      # unit axes of both kinds
+    ("(a,c,b),(b,a),(b)->(b)", dict(a=64, c=256, b=256), np.float32),  # block-per-output gathers
+])
+def test_coalesced_axes_bit_exact(dev, text, ext, dtype):
+    """Neighbouring axes every input walks as one are merged (and unit axes
+    dropped) before kernel selection; the merged walk visits the reduction
+    points in the reference's order, so results stay bit-identical, c0
+    included."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(31)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(dtype) for t in s.inputs]
+    init = rng.standard_normal([ext[a] for a in s.output]).astype(dtype)
+    want = np.asarray(oracle.generic(s.inputs, s.output, ins, init))
+    got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                   c0=torch.from_numpy(init).to(dev)).cpu().numpy()
+    uint = np.uint32 if dtype == np.float32 else np.uint64
+    assert np.array_equal(got.reshape(-1).view(uint), want.reshape(-1).view(uint)), text
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(c),(a,c),(b)->(c,a,b)", dict(c=8, a=64, b=512)),   # two broadcasts and a row vector
+    ("(a),(b)->(a,b)", dict(a=300, b=1024)),              # outer product
+    ("(a,b),(b)->(a,b)", dict(a=33, b=4096)),             # row scaling
+    ("(b,a),(b)->(a,b)", dict(a=128, b=256)),             # transposed (strided) operand
+])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64, torch.bfloat16])
+def test_broadcast_elementwise_bit_exact(dev, text, ext, dtype):
+    """Elementwise bodies with broadcast / strided operands run V outputs per
+    thread with 16-byte stores (bcast_ew_kernel): the same per-element
+    arithmetic as the loop nest (product, then + c0), checked bit for bit
+    against the oracle (f32/f64) and against the loop nest itself (bf16)."""
+    s = E.parse_einsum(text)
+    g = torch.Generator().manual_seed(37)
+    ins = [torch.randn([ext[a] for a in t], generator=g, dtype=torch.float64).to(dtype) for t in s.inputs]
+    init = torch.randn([ext[a] for a in s.output], generator=g, dtype=torch.float64).to(dtype)
+    got = contract(text, *[x.to(dev) for x in ins], c0=init.to(dev)).cpu()
+    if dtype == torch.bfloat16:
+        # reference arithmetic for 16-bit elementwise bodies: f32 products and add, one rounding
+        ref = _ew_f32(s, ext, [x.float() for x in ins]) + init.float()
+        assert torch.equal(got, ref.to(torch.bfloat16)), text
+    else:
+        want = np.asarray(oracle.generic(s.inputs, s.output, [x.numpy() for x in ins], init.numpy()))
+        uint = np.uint32 if dtype == torch.float32 else np.uint64
+        assert np.array_equal(got.numpy().reshape(-1).view(uint), want.reshape(-1).view(uint)), text
+
+
+def _ew_f32(s, ext, xs):
+    """Left-fold product of the operands broadcast to the output axes, in f32."""
+    out = None
+    for t, x in zip(s.inputs, xs):
+        perm = [t.index(a) for a in s.output if a in t]
+        y = x.permute(*perm) if perm else x
+        shape = [ext[a] if a in t else 1 for a in s.output]
+        y = y.reshape(shape)
+        out = y if out is None else out * y
+    return out.expand([ext[a] for a in s.output])
