@@ -423,4 +423,51 @@ __host__ __device__ __forceinline__ uint32_t make_idesc_tf32(bool a_mn_major, bo
   return d;
 }
 
+// Drop extent-1 axes and merge neighbouring axes of the same kind (parallel
+// with parallel, reduction with reduction) that every input walks as one:
+// stride[a] == extent[a+1] * stride[a+1].  The output is dense row-major over
+// the parallel axes, so merging them never changes an output address, and a
+// merged reduction axis visits the points in the same order — the reference's
+// loop nest, bit for bit.  (d,b,a)->(a) with (d,b) contiguous becomes a
+// single-axis column reduction and takes colchain_kernel (exact) or the
+// column tree layout (tolerance mode); BGX_NO_COALESCE=1 for A/B.
+inline bgx_generic_desc coalesce_axes(const bgx_generic_desc &d) {
+  static const bool off = getenv("BGX_NO_COALESCE") != nullptr;
+  if (off) return d;
+  for (int a = 0; a < d.n_axes; ++a)
+    if (d.extents[a] == 0) return d;
+  bgx_generic_desc w = d;
+  int n = 0, n_par = 0;
+  for (int a = 0; a < d.n_axes; ++a) {
+    const bool par = a < d.n_par;
+    if (d.extents[a] == 1) continue;
+    // merge into the previous kept axis when it is the same kind and contiguous with this one
+    if (n > 0 && (par == (n - 1 < n_par))) {
+      bool ok = true;
+      for (int k = 0; k < d.n_in && ok; ++k) ok = w.strides[k][n - 1] == d.extents[a] * d.strides[k][a];
+      if (ok) {
+        w.extents[n - 1] *= d.extents[a];
+        for (int k = 0; k < d.n_in; ++k) w.strides[k][n - 1] = d.strides[k][a];
+        continue;
+      }
+    }
+    w.extents[n] = d.extents[a];
+    for (int k = 0; k < d.n_in; ++k) w.strides[k][n] = d.strides[k][a];
+    ++n;
+    if (par) ++n_par;
+  }
+  if (n == 0) return d;
+  if (n == n_par && d.n_axes > d.n_par) {
+    // every reduction axis had extent 1: keep one, so the body still adds
+    // its single point to c0 (a one-input body without reduction axes is a
+    // plain copy)
+    w.extents[n] = 1;
+    for (int k = 0; k < d.n_in; ++k) w.strides[k][n] = 0;
+    ++n;
+  }
+  w.n_axes = n;
+  w.n_par = n_par;
+  return w;
+}
+
 }  // namespace bgx

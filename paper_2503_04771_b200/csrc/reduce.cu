@@ -632,8 +632,9 @@ int tree_splits(int64_t units, int64_t red, TreeLayout lay) {
 }
 
 template <typename S, typename T>
-int launch_tree(const bgx_generic_desc &d, int64_t n_out, int64_t red, void *ws,
+int launch_tree(const bgx_generic_desc &d0, int64_t n_out, int64_t red, void *ws,
                 int64_t ws_bytes, cudaStream_t s) {
+  const bgx_generic_desc d = coalesce_axes(d0);   // same merge as the workspace plan
   TreeLayout lay = tree_layout(d);
   if (d.n_in > 3 && lay != TreeLayout::General) lay = TreeLayout::General;
   const int64_t units = tree_units(d, lay, n_out);
@@ -734,10 +735,11 @@ extern "C" int bgx_generic_tree_plan(const bgx_generic_desc *d, int64_t *workspa
   int64_t n_out, red;
   const int rc = tree_check(d, &n_out, &red);
   if (rc != BGX_OK) return rc;
-  TreeLayout lay = tree_layout(*d);
-  if (d->n_in > 3 && lay != TreeLayout::General) lay = TreeLayout::General;
+  const bgx_generic_desc c = coalesce_axes(*d);
+  TreeLayout lay = tree_layout(c);
+  if (c.n_in > 3 && lay != TreeLayout::General) lay = TreeLayout::General;
   const int splits =
-      (n_out > 0 && red > 0) ? tree_splits(tree_units(*d, lay, n_out), red, lay) : 1;
+      (n_out > 0 && red > 0) ? tree_splits(tree_units(c, lay, n_out), red, lay) : 1;
   const int64_t esz = d->dtype == BGX_F64 ? 8 : 4;
   *workspace_bytes = splits > 1 ? n_out * splits * esz : 0;
   return BGX_OK;

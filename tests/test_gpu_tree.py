@@ -23,6 +23,10 @@ CASES = [
     ("(b,i,j)->(b)", [(6, 300, 500)]),
     ("(i,j,k)->(j)", [(40, 37, 300)]),
     ("(i,j),(i,j)->()", [(1000, 999), (1000, 999)]),
+    # merged axes (coalesce_axes): (d,b) -> one column axis, (a,b,c) -> one
+    ("(d,b,a)->(a)", [(300, 8, 1024)]),
+    ("(a,b,c,d)->(d)", [(32, 64, 16, 512)]),
+    ("(a,k,b),(k)->(a,b)", [(1, 5000, 64), (5000,)]),
 ]
 
 
