@@ -254,6 +254,37 @@ def _materialize_transposed(spec: EinsumSpec, inputs, out):
     return _spec_of(new_tups, spec.output), new_ins
 
 
+def _tree_output_order(spec, inputs):
+    """(spec with the output axes reordered, permutation back to the
+    requested order) when the largest input's unit-stride axis is an output
+    axis other than the innermost one — e.g. (d,a,b),(b)->(b,d) — and the
+    reduction is long enough for the extra move of the result not to matter;
+    else None."""
+    if len(spec.axes) == len(spec.output) or len(spec.output) < 2:
+        return None
+    k = max(range(len(inputs)), key=lambda i: inputs[i].numel())
+    x = inputs[k]
+    tup = spec.inputs[k]
+    unit = [a for d, a in enumerate(tup) if x.shape[d] > 1 and x.stride(d) == 1]
+    if not unit or unit[0] not in spec.output or unit[0] == spec.output[-1]:
+        return None
+    inner = spec.output[-1]
+    if inner in tup and x.stride(tup.index(inner)) == 1:
+        return None
+    n_out = 1
+    for a in spec.output:
+        for t, y in zip(spec.inputs, inputs):
+            if a in t:
+                n_out *= y.shape[t.index(a)]
+                break
+    if x.numel() < 16 * n_out:
+        return None
+    new_out = tuple(a for a in spec.output if a != unit[0]) + (unit[0],)
+    text = ",".join("(" + ",".join(t) + ")" for t in spec.inputs) + "->(" + ",".join(new_out) + ")"
+    from .einsum import parse_einsum
+    return parse_einsum(text), [new_out.index(a) for a in spec.output]
+
+
 def _fast_generic(spec, inputs, c0, out, tree: bool):
     """Pre-built descriptor for a repeated generic signature: later calls
     patch the pointers and launch (the planning, extents and Python
@@ -727,6 +758,19 @@ def execute(spec: EinsumSpec, inputs, c0: torch.Tensor | None, out: torch.Tensor
                 if a not in spec.output:
                     red_pts *= e
             tree = red_pts >= TREE_16BIT_POINTS
+        if tree:
+            ro = _tree_output_order(spec, inputs)
+            if ro is not None:
+                # the tree kernels' column layout needs the streamed input's
+                # contiguous axis innermost in the OUTPUT: reduce into that
+                # order, then move the (small) result
+                spec2, to_out = ro
+                ext = extents_of(spec, [t.shape for t in inputs])
+                tmp = torch.empty([ext[a] for a in spec2.output], dtype=dt, device=out.device)
+                c0p = None if c0 is None else \
+                    c0.permute([spec.output.index(a) for a in spec2.output]).contiguous()
+                generic(spec2, inputs, c0p, tmp, tree=True)
+                return permute(tmp, out, to_out)
         if out.is_contiguous():
             generic(spec, inputs, c0, out, tree=tree)
             if key is not None and not _transposed_inputs(spec, inputs, out):

@@ -27,6 +27,8 @@ CASES = [
     ("(d,b,a)->(a)", [(300, 8, 1024)]),
     ("(a,b,c,d)->(d)", [(32, 64, 16, 512)]),
     ("(a,k,b),(k)->(a,b)", [(1, 5000, 64), (5000,)]),
+    # output reordered so the input's unit-stride axis is innermost, then moved
+    ("(d,a,b),(b)->(b,d)", [(96, 300, 256), (256,)]),
 ]
 
 
@@ -135,3 +137,20 @@ def test_tolerance_paths_fuzz(dev, dt, mode):
         den = np.linalg.norm(np.atleast_1d(want))
         assert num <= tol * max(den, 1e-30), (text, ext, num / den)
         done += 1
+
+
+@pytest.mark.parametrize("dt,mode", [(torch.float32, "ffma"), (torch.bfloat16, "auto")])
+def test_tree_reordered_output_with_c0(dev, dt, mode):
+    """Tree reductions whose streamed input is contiguous along an outer
+    output axis run in the column layout on a reordered output and are moved
+    back (executor._tree_output_order); c0 follows the same permutation."""
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.randn(128, 2048, 256, device=dev, generator=g).to(dt)
+    v = torch.randn(256, device=dev, generator=g).to(dt)
+    c0 = torch.randn(256, 128, device=dev, generator=g).to(dt)
+    y = contract("(d,a,b),(b)->(b,d)", x, v, c0=c0, mode=mode)
+    assert y.shape == (256, 128)
+    want = _want("(d,a,b),(b)->(b,d)", [x, v], c0)
+    tol = 1e-5 if dt == torch.float32 else 2e-2
+    err = np.abs(y.double().cpu().numpy() - want).max() / np.abs(want).max()
+    assert err <= tol, err
