@@ -221,28 +221,73 @@ dense_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
 // output) was the cost: 33.5M-output outer product 229 us ~ 0.6 TB/s.
 // Same per-element arithmetic as generic_kernel: p = left fold of products,
 // out = p + c0 (or + 0).
+// one 16-byte vector of outputs: operand loads (bcast_ew_load) kept apart
+// from the product / c0 / store (bcast_ew_store) so several vectors' loads
+// can be in flight before the first store (stores may alias the inputs as
+// far as the compiler knows)
 template <typename S, typename T, int NIN>
-__global__ void __launch_bounds__(256) bcast_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
+__device__ __forceinline__ void bcast_ew_load(const bgx_generic_desc &d, const int64_t (&off)[NIN],
+                                              const int64_t (&sin)[NIN], T (&v)[NIN][16 / sizeof(S)]) {
   constexpr int V = 16 / (int)sizeof(S);
   const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+#pragma unroll
+  for (int k = 0; k < NIN; ++k) {
+    const S *src = ins[k] + off[k];
+    if (sin[k] == 0) {
+      const T x = ld_as<S, T>(src);
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[k][e] = x;
+    } else if (sin[k] == 1 && ((uintptr_t)src & 15) == 0) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(src);   // may be reused across rows
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[k][e] = ld_as<S, T>(reinterpret_cast<const S *>(&q) + e);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[k][e] = ld_as<S, T>(src + e * sin[k]);
+    }
+  }
+}
+
+template <typename S, typename T, int NIN>
+__device__ __forceinline__ void bcast_ew_store(const bgx_generic_desc &d, const T (&v)[NIN][16 / sizeof(S)],
+                                               int64_t o) {
+  constexpr int V = 16 / (int)sizeof(S);
   const S *c0 = static_cast<const S *>(d.c0);
-  S *out = static_cast<S *>(d.out);
+  const uint4 cq = c0 ? __ldcs(reinterpret_cast<const uint4 *>(c0 + o)) : make_uint4(0, 0, 0, 0);
+  uint4 r;
+  S *re = reinterpret_cast<S *>(&r);
+#pragma unroll
+  for (int e = 0; e < V; ++e) {
+    T p = v[0][e];
+#pragma unroll
+    for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, v[k][e]);
+    const T acc = c0 ? ld_as<S, T>(reinterpret_cast<const S *>(&cq) + e) : T(0);
+    re[e] = st_as<S, T>(add_rn<T>(p, acc));
+  }
+  __stcs(reinterpret_cast<uint4 *>(static_cast<S *>(d.out) + o), r);
+}
+
+// Elementwise bodies with broadcast or strided operands (outer products,
+// scalings, (c),(a,c),(b)->(c,a,b)): the output is dense, so work goes by
+// 16-byte vectors of consecutive outputs along the innermost output axis.
+// ROWS (rows of >= 32 vectors): a warp walks whole rows, decoding each row
+// once; otherwise a thread decodes every vector.  Operands load as one 16-byte vector (unit stride, aligned), one
+// broadcast scalar (stride 0) or V strided scalars.  The per-output decode
+// of generic_kernel (a division per axis per output) was the cost:
+// 33.5M-output outer product 229 us ~ 0.6 TB/s.  Same per-element
+// arithmetic as generic_kernel: p = left fold of products, out = p + c0 (or + 0).
+template <typename S, typename T, int NIN, bool ROWS>
+__global__ void __launch_bounds__(256) bcast_ew_kernel(const bgx_generic_desc d, int64_t n_out) {
+  constexpr int V = 16 / (int)sizeof(S);
   const int np = d.n_par;
   const int64_t E = d.extents[np - 1];
   int64_t sin[NIN];
 #pragma unroll
   for (int k = 0; k < NIN; ++k) sin[k] = d.strides[k][np - 1];
-  const int64_t nv = n_out / V;
   const bool idx32 = n_out <= 0x7fffffffLL;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = i * V;
-    int64_t row, j;
-    if (idx32) { row = (uint32_t)o / (uint32_t)E; j = (uint32_t)o - (uint32_t)row * (uint32_t)E; }
-    else { row = o / E; j = o - row * E; }
-    int64_t off[NIN];
+  auto decode_row = [&](int64_t row, int64_t (&off)[NIN]) {
 #pragma unroll
-    for (int k = 0; k < NIN; ++k) off[k] = j * sin[k];
+    for (int k = 0; k < NIN; ++k) off[k] = 0;
     if (idx32) {
       uint32_t rem = (uint32_t)row;
       for (int a = np - 2; a >= 0; --a) {
@@ -260,35 +305,53 @@ __global__ void __launch_bounds__(256) bcast_ew_kernel(const bgx_generic_desc d,
         for (int k = 0; k < NIN; ++k) off[k] += x * d.strides[k][a];
       }
     }
-    T v[NIN][V];
+  };
+  if constexpr (ROWS) {
+    // a warp walks whole rows (one decode per row); each lane issues the
+    // operand loads of U vectors before their stores
+    constexpr int U = sizeof(S) == 2 ? 2 : 4;
+    const int lane = threadIdx.x % 32;
+    const int64_t nrows = n_out / E, vpr = E / V;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+    for (int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; row < nrows;
+         row += warps) {
+      int64_t base[NIN];
+      decode_row(row, base);
+      for (int64_t j0 = lane; j0 < vpr; j0 += 32 * U) {
+        T v[U][NIN][V];
 #pragma unroll
-    for (int k = 0; k < NIN; ++k) {
-      const S *src = ins[k] + off[k];
-      if (sin[k] == 0) {
-        const T x = ld_as<S, T>(src);
+        for (int u = 0; u < U; ++u) {
+          const int64_t jv = j0 + 32 * u;
+          if (jv < vpr) {
+            int64_t off[NIN];
 #pragma unroll
-        for (int e = 0; e < V; ++e) v[k][e] = x;
-      } else if (sin[k] == 1 && ((uintptr_t)src & 15) == 0) {
-        const uint4 q = *reinterpret_cast<const uint4 *>(src);
+            for (int k = 0; k < NIN; ++k) off[k] = base[k] + jv * V * sin[k];
+            bcast_ew_load<S, T, NIN>(d, off, sin, v[u]);
+          }
+        }
 #pragma unroll
-        for (int e = 0; e < V; ++e) v[k][e] = ld_as<S, T>(reinterpret_cast<const S *>(&q) + e);
-      } else {
-#pragma unroll
-        for (int e = 0; e < V; ++e) v[k][e] = ld_as<S, T>(src + e * sin[k]);
+        for (int u = 0; u < U; ++u) {
+          const int64_t jv = j0 + 32 * u;
+          if (jv < vpr) bcast_ew_store<S, T, NIN>(d, v[u], row * E + jv * V);
+        }
       }
     }
-    uint4 cq = c0 ? *reinterpret_cast<const uint4 *>(c0 + o) : make_uint4(0, 0, 0, 0);
-    uint4 r;
-    S *re = reinterpret_cast<S *>(&r);
+  } else {
+    const int64_t nv = n_out / V;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t o = i * V;
+      int64_t row, j;
+      if (idx32) { row = (uint32_t)o / (uint32_t)E; j = (uint32_t)o - (uint32_t)row * (uint32_t)E; }
+      else { row = o / E; j = o - row * E; }
+      int64_t off[NIN];
+      decode_row(row, off);
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      T p = v[0][e];
-#pragma unroll
-      for (int k = 1; k < NIN; ++k) p = mul_rn<T>(p, v[k][e]);
-      const T acc = c0 ? ld_as<S, T>(reinterpret_cast<const S *>(&cq) + e) : T(0);
-      re[e] = st_as<S, T>(add_rn<T>(p, acc));
+      for (int k = 0; k < NIN; ++k) off[k] += j * sin[k];
+      T v[NIN][V];
+      bcast_ew_load<S, T, NIN>(d, off, sin, v);
+      bcast_ew_store<S, T, NIN>(d, v, o);
     }
-    __stcs(reinterpret_cast<uint4 *>(out + o), r);
   }
 }
 
@@ -1215,8 +1278,25 @@ int launch_generic(const bgx_generic_desc &d0, int64_t n_out, int64_t red, cudaS
     int64_t vb = (n_out / (16 / (int64_t)sizeof(S)) + 255) / 256;
     if (vb > (int64_t)sms * 16) vb = (int64_t)sms * 16;
     if (vb < 1) vb = 1;
-    if (d.n_in == 2) bcast_ew_kernel<S, T, 2><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
-    else bcast_ew_kernel<S, T, 3><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+    static const bool no_rows = getenv("BGX_BCAST_NO_ROWS") != nullptr;   // A/B only
+    // rows of at least 32 x U vectors (U = 4, 2 for 16-bit; shorter rows idle
+    // lanes) and enough rows for 16 warps per SM (256 rows of 65536: 2.6x
+    // slower than one decode per vector)
+    const bool rows = !no_rows &&
+                      d.extents[d.n_par - 1] / (16 / (int64_t)sizeof(S)) >= (sizeof(S) == 2 ? 64 : 128) &&
+                      n_out / d.extents[d.n_par - 1] >= 16 * (int64_t)sms;
+    if (rows) {
+      const int64_t nrows = n_out / d.extents[d.n_par - 1];
+      int64_t rb = (nrows + 7) / 8;   // 8 warps per block, a row per warp
+      if (rb > (int64_t)sms * 16) rb = (int64_t)sms * 16;
+      if (rb < 1) rb = 1;
+      if (d.n_in == 2) bcast_ew_kernel<S, T, 2, true><<<(unsigned)rb, 256, 0, s>>>(d, n_out);
+      else bcast_ew_kernel<S, T, 3, true><<<(unsigned)rb, 256, 0, s>>>(d, n_out);
+    } else if (d.n_in == 2) {
+      bcast_ew_kernel<S, T, 2, false><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+    } else {
+      bcast_ew_kernel<S, T, 3, false><<<(unsigned)vb, 256, 0, s>>>(d, n_out);
+    }
     return check_launch("bcast_ew_kernel");
   }
   if (dense) {

@@ -163,7 +163,7 @@ SMALL_BATCHED_GEMM = True      # A/B switch
 SMALL_BATCHED_MN = 1024        # output elements per batch entry (<= 32 x 32), f32/f64
 SMALL_BATCHED_MN_16BIT = 256   # 16-bit: the tensor-core tiles win from 32 x 32 up
 SMALL_BATCHED_K = 256
-OUTER_TO_LOOP_NEST = False     # A/B switches (outer products: the GEMM tiles measured 2-4x faster)
+OUTER_TO_LOOP_NEST = True      # A/B switches (outer products: the broadcast elementwise kernel, 1-4x faster than K = 1 GEMM tiles, scripts/r02/outer_ab.py)
 SKINNY_TO_LOOP_NEST = True
 SKINNY_MN = 8
 
@@ -232,9 +232,9 @@ def _plan_generic(spec: EinsumSpec, shapes, strides, *, dtype: str, mode: str = 
         return GenericPlan("small batched GEMM")
     if not k and OUTER_TO_LOOP_NEST:
         # no reduction at all (outer products included): every output is one
-        # product, written once — the loop nest / elementwise kernels move
-        # the bytes; a GEMM tile with K = 1 spent 3-4x the write time
-        # (scripts/r02/shape_audit.py)
+        # product, written once — the broadcast elementwise kernel
+        # (bcast_ew_kernel) moves the bytes; GEMM tiles with K = 1 were equal
+        # to 4x slower (scripts/r02/outer_ab.py, profiles/r02_exact_chains.txt)
         return GenericPlan("outer / elementwise product (no reduction)")
     if ref_types and k and SKINNY_TO_LOOP_NEST and (
             _prod(ext[a] for a in m) <= SKINNY_MN or _prod(ext[a] for a in n) <= SKINNY_MN):
