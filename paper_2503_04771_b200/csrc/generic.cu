@@ -1203,9 +1203,11 @@ __global__ void __launch_bounds__(CH_THREADS) chain_general_kernel(const bgx_gen
       const T *x = buf[t & 1];
       const int64_t n = red - t * CG_TILE < CG_TILE ? red - t * CG_TILE : CG_TILE;
       int64_t e = 0;
-      if (n == CG_TILE) {
-        acc = fold16<T, 1>(x, nullptr, CG_TILE * (int)sizeof(T) / 16, acc);
-        e = CG_TILE;
+      // whole groups of 4 16-byte vectors pipelined, the rest one by one
+      const int nv = (int)(n * (int64_t)sizeof(T) / 16) / 4 * 4;
+      if (nv > 0) {
+        acc = fold16<T, 1>(x, nullptr, nv, acc);
+        e = (int64_t)nv * (16 / (int)sizeof(T));
       }
       for (; e < n; ++e) acc = add_rn<T>(x[e], acc);
     }
@@ -1224,6 +1226,38 @@ bool try_chain_general(const bgx_generic_desc &d, int64_t n_out, int64_t red, cu
   if (n_out < 1 || n_out > 4 * (int64_t)(sms > 0 ? sms : 148) || red < 2 * cg_tile<T>() ||
       d.n_in < 1 || d.n_axes <= d.n_par)
     return false;
+  chain_general_kernel<T><<<(unsigned)n_out, CH_THREADS, 0, s>>>(d, red);
+  *rc = check_launch("chain_general_kernel");
+  return true;
+}
+
+// What the row / column kernels left for the per-thread loop nest, when that
+// walk cannot coalesce (no parallel axis moves the largest operand at unit
+// stride: each thread streams its own run, a warp load touches 32 lines):
+// block-per-output chains for up to 32 outputs per SM and reductions of at
+// least 1024 points, whose producer warps read each output's points
+// contiguously: (b,a,c),(c,a)->(b) 2048 x 4096 points 291 -> 104 us,
+// (d,a,c),(c,a),(c)->(d) 4096 x 2048 159 -> 138 us; with more outputs or
+// shorter chains the per-block cost loses to the loop nest (8192 x 2048:
+// 151 -> 225 us, scripts/r02/cg_wide_ab.sh).  BGX_NO_CG_WIDE=1 for A/B.
+template <typename T>
+bool try_chain_general_wide(const bgx_generic_desc &d, int64_t n_out, int64_t red, cudaStream_t s,
+                            int *rc) {
+  static const bool off = getenv("BGX_NO_CG_WIDE") != nullptr;
+  const int sms = sm_count_current();
+  if (off || n_out < 1 || n_out > 32 * (int64_t)(sms > 0 ? sms : 148) || red < 1024 || d.n_in < 1 ||
+      d.n_axes <= d.n_par || n_out > 0x7fffffffLL)
+    return false;
+  int big = 0;
+  int64_t bigsz = -1;
+  for (int k = 0; k < d.n_in; ++k) {
+    int64_t sz = 1;   // elements the operand spans (product of the extents it moves along)
+    for (int a = 0; a < d.n_axes; ++a)
+      if (d.strides[k][a] != 0) sz *= d.extents[a];
+    if (sz > bigsz) { bigsz = sz; big = k; }
+  }
+  for (int a = 0; a < d.n_par; ++a)
+    if (d.extents[a] > 1 && (d.strides[big][a] == 1 || d.strides[big][a] == -1)) return false;
   chain_general_kernel<T><<<(unsigned)n_out, CH_THREADS, 0, s>>>(d, red);
   *rc = check_launch("chain_general_kernel");
   return true;
@@ -1256,6 +1290,7 @@ int launch_generic(const bgx_generic_desc &d0, int64_t n_out, int64_t red, cudaS
     if (!no_rr && try_chain<T>(d, n_out, red, s, &rc)) return rc;
     if (!no_rr && try_chain_general<T>(d, n_out, red, s, &rc)) return rc;
     if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
+    if (!no_rr && try_chain_general_wide<T>(d, n_out, red, s, &rc)) return rc;
   }
   if (dense && d.n_in >= 2 && d.n_in <= 3 && red == 1) {
     bool aligned = ((uintptr_t)d.out % 16 == 0) && ((uintptr_t)d.c0 % 16 == 0);

@@ -431,3 +431,24 @@ def _ew_f32(s, ext, xs):
         y = y.reshape(shape)
         out = y if out is None else out * y
     return out.expand([ext[a] for a in s.output])
+
+
+@pytest.mark.parametrize("text,ext,dtype", [
+    ("(b,a,c),(c,a)->(b)", dict(b=300, a=32, c=64), np.float32),           # operand transposed vs the walk
+    ("(d,a,c),(c,a),(c)->(d)", dict(d=200, a=8, c=160), np.float64),       # three operands, 1280-point chains
+    ("(b,a,c),(c,a)->(b)", dict(b=64, a=33, c=37), np.float32),            # ragged last tile
+])
+def test_block_chains_for_uncoalesced_walks_bit_exact(dev, text, ext, dtype):
+    """Reductions the row / column kernels cannot take and the per-thread
+    loop nest cannot coalesce run as block-per-output chains (producer warps
+    read each output's points contiguously, one thread folds them in order):
+    bit-identical to the reference order, c0 included."""
+    s = E.parse_einsum(text)
+    rng = np.random.default_rng(41)
+    ins = [rng.standard_normal([ext[a] for a in t]).astype(dtype) for t in s.inputs]
+    init = rng.standard_normal([ext[a] for a in s.output]).astype(dtype)
+    want = np.asarray(oracle.generic(s.inputs, s.output, ins, init))
+    got = contract(text, *[torch.from_numpy(x).to(dev) for x in ins],
+                   c0=torch.from_numpy(init).to(dev)).cpu().numpy()
+    uint = np.uint32 if dtype == np.float32 else np.uint64
+    assert np.array_equal(got.reshape(-1).view(uint), want.reshape(-1).view(uint)), text
