@@ -426,7 +426,7 @@ def _launch(lib, d, kind, splits, ws_bytes, out) -> int:
 
 PAD_MIN_FLOP = 1 << 28
 TREE_16BIT_POINTS = 1024
-PREREDUCE_16BIT_BLOWUP = 64
+PREREDUCE_16BIT_BLOWUP = 16   # product space vs operands; 64 left the perf fuzz's 2^30-2^31-point bf16 bodies (32-64x) on an 8-20 ms direct walk
 
 
 def _contract_padded(a, a_strides, b, b_strides, out, o_strides, *, batch, M, N, K, c0,

@@ -83,3 +83,28 @@ def test_small_multi_operand_16bit_bodies_round_once(dev, text, ext):
     tt = ",".join("".join(t) for t in s.inputs) + "->" + "".join(s.output)
     want = torch.einsum(tt, *[x.double() for x in xs])
     assert ((got - want).norm() / want.norm()).item() <= 1e-2
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(a,c,d),(b)->()", dict(a=512, c=8, d=256, b=64)),           # both operands fully private
+    ("(a,c,d),(b,c,a)->()", dict(a=64, c=256, d=64, b=64)),       # 32x blow-up: pre-reduced
+    ("(a,d),(c,a,b)->(c,d)", dict(c=32, d=32, a=64, b=512)),
+])
+def test_16bit_prereduced_private_axes_accuracy(dev, text, ext):
+    """16-bit tolerance bodies whose product space is >= 16x the operands sum
+    each operand over its private reduction axes first (one extra 16-bit
+    rounding of the partial sums, as torch.einsum's pairwise contraction
+    stores them): within 2e-2 of the f64 sum on positive data."""
+    s = E.parse_einsum(text)
+    g = torch.Generator(device=dev).manual_seed(5)
+    xs = [torch.rand([ext[a] for a in t], generator=g, device=dev).to(torch.bfloat16) for t in s.inputs]
+    executor.reset_launch_log()
+    got = contract(text, *xs).double()
+    kinds = executor.launch_log()
+    assert len(kinds) >= 2, kinds                                    # the pre-reductions ran
+    letters = {a: chr(97 + n) for n, a in enumerate(s.axes)}
+    eq = ",".join("".join(letters[a] for a in t) for t in s.inputs) + "->" + \
+        "".join(letters[a] for a in s.output)
+    want = torch.einsum(eq, *[x.double() for x in xs])
+    err = ((got - want).abs().max() / want.abs().max()).item()
+    assert err <= 2e-2, err
