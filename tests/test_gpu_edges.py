@@ -452,3 +452,17 @@ def test_block_chains_for_uncoalesced_walks_bit_exact(dev, text, ext, dtype):
                    c0=torch.from_numpy(init).to(dev)).cpu().numpy()
     uint = np.uint32 if dtype == np.float32 else np.uint64
     assert np.array_equal(got.reshape(-1).view(uint), want.reshape(-1).view(uint)), text
+
+
+def test_cached_transposed_elementwise_repeat_calls_bit_exact(dev):
+    """A repeated elementwise signature whose input is materialised in the
+    output's axis order runs from the cached launcher (copy + one launch);
+    every call sees its own data, bit for bit."""
+    g = torch.Generator(device=dev).manual_seed(43)
+    outs = torch.empty(2048, 1024, device=dev)
+    for _ in range(3):
+        x = torch.randn(1024, 2048, device=dev, generator=g)
+        v = torch.randn(1024, device=dev, generator=g)
+        got = contract("(b,c),(b)->(c,b)", x, v, out=outs)
+        want = (x * v[:, None]).t() + 0.0
+        assert torch.equal(got, want)
