@@ -485,18 +485,18 @@ template <typename T> constexpr int rr_stride(bool vec, int tj = RR_TJ) {
 
 // NW warps per block, ST tiles in flight per warp, TJ columns per tile.
 template <typename T, int NIN, bool COLS, bool VEC = false, int NW = RR_WARPS, int ST = RR_STAGES,
-          int TJ = RR_TJ>
+          int TJ = RR_TJ, typename S = T>
 __global__ void __launch_bounds__(32 * NW)
 rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) {
   // shared_mask bit k: input k does not depend on the output index (e.g. the
   // vector of a GEMV): its tile row is loaded once and read by every lane
   // tile[stage][input][row][col], +1 column of padding against bank conflicts
   extern __shared__ __align__(16) uint8_t rr_smem_raw[];
-  T *tiles = reinterpret_cast<T *>(rr_smem_raw);
+  S *tiles = reinterpret_cast<S *>(rr_smem_raw);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  constexpr int RS = rr_stride<T>(VEC, TJ);          // tile row stride (elements)
+  constexpr int RS = rr_stride<S>(VEC, TJ);          // tile row stride (elements)
   constexpr int TSZ = 32 * RS;                    // one tile
-  T *wtiles = tiles + (size_t)warp * ST * NIN * TSZ;
+  S *wtiles = tiles + (size_t)warp * ST * NIN * TSZ;
   const int n_par = d.n_par;
   const int64_t E = d.extents[d.n_axes - 1];
   const int64_t o0 = ((int64_t)blockIdx.x * NW + warp) * 32;
@@ -518,13 +518,13 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
       for (int k = 0; k < NIN; ++k) off[k] += i * d.strides[k][a];
     }
   }
-  const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
+  const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
   const int64_t ntiles = (E + TJ - 1) / TJ;
   // VEC staging: the source of each (row group i, vector) this lane copies
-  constexpr int VE16 = 16 / (int)sizeof(T);
+  constexpr int VE16 = 16 / (int)sizeof(S);
   constexpr int VRPI = VEC ? 32 / (TJ / VE16) : 1;
   constexpr int VG = VEC ? 32 / VRPI : 1;            // row groups per tile
-  const T *vsrc[NIN][VG];
+  const S *vsrc[NIN][VG];
   bool vrow_ok[VG];
   if constexpr (VEC) {
     const int v = lane % (TJ / VE16);
@@ -544,7 +544,7 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     const int64_t j = t * TJ + lane;          // this lane's column of the tile
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
-      T *tile = wtiles + (stage * NIN + k) * TSZ;
+      S *tile = wtiles + (stage * NIN + k) * TSZ;
       if ((shared_mask >> (8 + k)) & 1) {
         // constant along the reduction (a per-output factor): never staged
       } else if (COLS && ((shared_mask >> k) & 1)) {
@@ -553,12 +553,12 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
         const int64_t sk = d.strides[k][d.n_axes - 1];
         const int64_t jj = t * TJ + lane;
         const bool ok = jj < E;
-        const T *src = ins[k] + (ok ? off[k] + jj * sk : 0);
-        if constexpr (sizeof(T) == 4) cp_async4(tile + lane, src, ok);
+        const S *src = ins[k] + (ok ? off[k] + jj * sk : 0);
+        if constexpr (sizeof(S) == 4) cp_async4(tile + lane, src, ok);
         else cp_async8(tile + lane, src, ok);
       } else if constexpr (VEC) {
         // rows of the tile as 16-byte vectors: lane -> (row, vector) pairs
-        constexpr int E16 = 16 / (int)sizeof(T);
+        constexpr int E16 = 16 / (int)sizeof(S);
         constexpr int VPR = TJ / E16;           // vectors per tile row
         static_assert(VPR <= 32 && 32 % VPR == 0, "a tile row must fit one warp instruction");
         constexpr int RPI = 32 / VPR;              // rows per instruction
@@ -567,21 +567,21 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
           // shared operand: one row, VPR lanes
           const int64_t jj = t * TJ + v * E16;
           const int64_t left = E - jj;
-          const int bytes = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
+          const int bytes = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(S) : 0);
           if (lane < VPR) cp_async16(tile + v * E16, ins[k] + (bytes ? off[k] + jj : 0), bytes);
         } else {
           // per-lane source pointers precomputed once (vsrc); a full tile of
           // 32 live rows is one pointer add + one cp.async per row group
           const bool full = (t + 1) * TJ <= E;
           if (full && all_rows) {
-            T *dst0 = tile + (lane / VPR) * RS + v * E16;
+            S *dst0 = tile + (lane / VPR) * RS + v * E16;
 #pragma unroll
             for (int i = 0; i < 32 / RPI; ++i)
               cp_async16_full(dst0 + i * RPI * RS, vsrc[k][i] + t * TJ);
           } else {
             const int64_t jj = t * TJ + v * E16;
             const int64_t left = E - jj;
-            const int tail = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(T) : 0);
+            const int tail = left >= E16 ? 16 : (left > 0 ? (int)left * (int)sizeof(S) : 0);
 #pragma unroll
             for (int i = 0; i < 32 / RPI; ++i) {
               const int rr = i * RPI + lane / VPR;
@@ -595,16 +595,16 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
         for (int rr = 0; rr < 32; ++rr) {
           const int64_t jj = t * TJ + rr;       // reduction step of this tile row
           const bool ok = row_ok && jj < E;
-          const T *src = ins[k] + (ok ? off[k] + jj * sk : 0);
-          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * RS + lane, src, ok);
+          const S *src = ins[k] + (ok ? off[k] + jj * sk : 0);
+          if constexpr (sizeof(S) == 4) cp_async4(tile + rr * RS + lane, src, ok);
           else cp_async8(tile + rr * RS + lane, src, ok);
         }
       } else {
         auto copy_row = [&](int rr) {
           const int64_t base = __shfl_sync(0xffffffffu, off[k], rr);
           const bool ok = (o0 + rr < n_out) && j < E;
-          const T *src = ins[k] + (ok ? base + j : 0);
-          if constexpr (sizeof(T) == 4) cp_async4(tile + rr * RS + lane, src, ok);
+          const S *src = ins[k] + (ok ? base + j : 0);
+          if constexpr (sizeof(S) == 4) cp_async4(tile + rr * RS + lane, src, ok);
           else cp_async8(tile + rr * RS + lane, src, ok);
         };
         if ((shared_mask >> k) & 1) {
@@ -616,13 +616,13 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     }
     cp_async_commit();
   };
-  T acc = (row_ok && d.c0) ? static_cast<const T *>(d.c0)[o] : T(0);
+  T acc = (row_ok && d.c0) ? ld_as<S, T>(static_cast<const S *>(d.c0) + o) : T(0);
   // operands constant along the reduction (shared_mask bits 8..15): one
   // value per lane, multiplied in at their place in the left fold
   T invv[NIN];
 #pragma unroll
   for (int k = 0; k < NIN; ++k)
-    invv[k] = (((shared_mask >> (8 + k)) & 1) && row_ok) ? ins[k][off[k]] : T(0);
+    invv[k] = (((shared_mask >> (8 + k)) & 1) && row_ok) ? ld_as<S, T>(ins[k] + off[k]) : T(0);
   for (int64_t t = 0; t < ST - 1; ++t) {
     if (t < ntiles) issue(t); else cp_async_commit();
   }
@@ -633,7 +633,7 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     const int stage = (int)(t % ST);
     const int jmax = (E - t * TJ) < TJ ? (int)(E - t * TJ) : TJ;
     // element c of this lane's chain: row layout tile[lane][c], column layout tile[c][lane]
-    const T *row[NIN];
+    const S *row[NIN];
     int cstep[NIN];
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
@@ -642,7 +642,7 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
       cstep[k] = (COLS && !sh) ? RS : 1;
     }
     if (VEC && jmax == TJ) {
-      constexpr int E16 = 16 / (int)sizeof(T);
+      constexpr int E16 = 16 / (int)sizeof(S);
 #pragma unroll 2
       for (int c4 = 0; c4 < TJ; c4 += E16) {
         T v[NIN][E16];
@@ -654,9 +654,9 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
             continue;
           }
           const uint4 q = *reinterpret_cast<const uint4 *>(row[k] + c4);
-          const T *e = reinterpret_cast<const T *>(&q);
+          const S *e = reinterpret_cast<const S *>(&q);
 #pragma unroll
-          for (int i = 0; i < E16; ++i) v[k][i] = e[i];
+          for (int i = 0; i < E16; ++i) v[k][i] = ld_as<S, T>(e + i);
         }
 #pragma unroll
         for (int i = 0; i < E16; ++i) {
@@ -669,25 +669,25 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
     } else if (jmax == TJ) {
 #pragma unroll 8
       for (int c = 0; c < TJ; ++c) {
-        T p = ((shared_mask >> 8) & 1) ? invv[0] : row[0][c * cstep[0]];
+        T p = ((shared_mask >> 8) & 1) ? invv[0] : ld_as<S, T>(row[0] + c * cstep[0]);
 #pragma unroll
         for (int k = 1; k < NIN; ++k)
-          p = mul_rn<T>(p, ((shared_mask >> (8 + k)) & 1) ? invv[k] : row[k][c * cstep[k]]);
+          p = mul_rn<T>(p, ((shared_mask >> (8 + k)) & 1) ? invv[k] : ld_as<S, T>(row[k] + c * cstep[k]));
         acc = add_rn<T>(p, acc);
       }
     } else {
       for (int c = 0; c < jmax; ++c) {
-        T p = ((shared_mask >> 8) & 1) ? invv[0] : row[0][c * cstep[0]];
+        T p = ((shared_mask >> 8) & 1) ? invv[0] : ld_as<S, T>(row[0] + c * cstep[0]);
 #pragma unroll
         for (int k = 1; k < NIN; ++k)
-          p = mul_rn<T>(p, ((shared_mask >> (8 + k)) & 1) ? invv[k] : row[k][c * cstep[k]]);
+          p = mul_rn<T>(p, ((shared_mask >> (8 + k)) & 1) ? invv[k] : ld_as<S, T>(row[k] + c * cstep[k]));
         acc = add_rn<T>(p, acc);
       }
     }
     __syncwarp();                                // stage free before it is refilled
   }
   cp_async_wait<0>();
-  if (row_ok) static_cast<T *>(d.out)[o] = acc;
+  if (row_ok) static_cast<S *>(d.out)[o] = st_as<S, T>(acc);
 }
 
 // ---- exact column chains, 16-byte staged ----------------------------------
@@ -880,11 +880,16 @@ bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int 
   return true;
 }
 
-template <typename T>
+// S: storage type (f32/f64, or bf16/f16 folded in f32: 16-byte staged rows
+// only — cp.async has no 2-byte copies)
+template <typename T, typename S = T>
 bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int *rc) {
+  constexpr bool same = std::is_same<S, T>::value;
   if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2 || d.n_par < 1) return false;
   const int ax = d.n_axes - 1, inner = d.n_par - 1;
-  if (try_colchain<T>(d, n_out, s, rc)) return true;
+  if constexpr (same) {
+    if (try_colchain<T>(d, n_out, s, rc)) return true;
+  }
   bool rows = true, cols = true;
   // rows mode may carry operands constant along the reduction (a per-output
   // factor, loaded once per lane) as long as one operand streams the row
@@ -915,7 +920,10 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     if ((inv_mask >> k) & 1) continue;
     vec = ((uintptr_t)d.ins[k] % 16) == 0;
     for (int a = 0; a < d.n_par && vec; ++a)
-      vec = d.extents[a] == 1 || (d.strides[k][a] * (int64_t)sizeof(T)) % 16 == 0;
+      vec = d.extents[a] == 1 || (d.strides[k][a] * (int64_t)sizeof(S)) % 16 == 0;
+  }
+  if constexpr (!same) {
+    if (!rows || !vec) return false;   // 16-bit storage: 16-byte staged rows only
   }
   // fewer outputs than 4 warps per SM: one-warp blocks, so every SM streams
   // (a warp's chains cannot be split across SMs)
@@ -936,19 +944,19 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   const bool thin_rows = thin && rows && vec;
   int tj = RR_TJ;
   if (thin_rows) {
-    tj = thin_tj_env ? thin_tj_env : (sizeof(T) == 4 ? 128 : 64);
+    tj = thin_tj_env ? thin_tj_env : (sizeof(S) <= 4 ? 128 : 64);
     if (tj != 32 && tj != 64 && tj != 128) tj = RR_TJ;
-    if (sizeof(T) == 8 && tj == 128) tj = 64;
+    if (sizeof(S) == 8 && tj == 128) tj = 64;
   }
   int st = thin_rows ? (tj == 128 ? 2 : tj == 64 ? 3 : RR_STAGES) : RR_STAGES;
   // many outputs, one f32 input: 64-column tiles, 2 in flight (5-12 % faster
   // than 32 x 4: fewer tile iterations per element; BGX_RR_NARROW=1 for A/B)
   static const bool narrow_env = getenv("BGX_RR_NARROW") != nullptr;
-  const bool wide4 = !narrow_env && !thin && rows && vec && d.n_in == 1 && sizeof(T) == 4;
+  const bool wide4 = !narrow_env && !thin && rows && vec && d.n_in == 1 && sizeof(S) <= 4;
   if (wide4) { tj = 64; st = 2; }
   const int64_t blocks = (n_out + 32 * nw - 1) / (32 * nw);
   if (blocks > 0x7fffffffLL) return false;
-  const size_t smem = (size_t)nw * st * d.n_in * 32 * rr_stride<T>(vec, tj) * sizeof(T);
+  const size_t smem = (size_t)nw * st * d.n_in * 32 * rr_stride<S>(vec, tj) * sizeof(S);
   if (smem > 200 * 1024) return false;
   uint32_t shared_mask = 0;
   for (int k = 0; k < d.n_in; ++k) {
@@ -962,27 +970,32 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
     set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
     kern<<<(unsigned)blocks, 32 * nw, smem, s>>>(d, n_out, shared_mask);
   };
-  constexpr bool f32 = sizeof(T) == 4;
+  constexpr bool f32 = sizeof(S) <= 4;   // 128-column tiles: f32 and 16-bit storage
   if (f32 && thin_rows && tj == 128) {
     if constexpr (f32) {
-      if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, 2, 128>);
-      else go(rowreduce_kernel<T, 2, false, true, 1, 2, 128>);
+      if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, 2, 128, S>);
+      else go(rowreduce_kernel<T, 2, false, true, 1, 2, 128, S>);
     }
   } else if (thin_rows && tj == 64) {
-    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, 3, 64>);
-    else go(rowreduce_kernel<T, 2, false, true, 1, 3, 64>);
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, 3, 64, S>);
+    else go(rowreduce_kernel<T, 2, false, true, 1, 3, 64, S>);
   } else if (thin_rows) {
-    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1>);
-    else go(rowreduce_kernel<T, 2, false, true, 1>);
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, 1, RR_STAGES, RR_TJ, S>);
+    else go(rowreduce_kernel<T, 2, false, true, 1, RR_STAGES, RR_TJ, S>);
   } else if (rows && vec && wide4) {
-    if constexpr (f32) go(rowreduce_kernel<T, 1, false, true, RR_WARPS, 2, 64>);
+    if constexpr (f32) go(rowreduce_kernel<T, 1, false, true, RR_WARPS, 2, 64, S>);
   } else if (rows && vec) {
-    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true>); else go(rowreduce_kernel<T, 2, false, true>);
+    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false, true, RR_WARPS, RR_STAGES, RR_TJ, S>);
+    else go(rowreduce_kernel<T, 2, false, true, RR_WARPS, RR_STAGES, RR_TJ, S>);
   } else if (rows) {
-    if (d.n_in == 1) go(rowreduce_kernel<T, 1, false>); else go(rowreduce_kernel<T, 2, false>);
+    if constexpr (same) {
+      if (d.n_in == 1) go(rowreduce_kernel<T, 1, false>); else go(rowreduce_kernel<T, 2, false>);
+    }
   } else {   // columns (few outputs: one-warp blocks over every SM)
-    if (d.n_in == 1) go(rowreduce_kernel<T, 1, true, false, 1>);
-    else go(rowreduce_kernel<T, 2, true, false, 1>);
+    if constexpr (same) {
+      if (d.n_in == 1) go(rowreduce_kernel<T, 1, true, false, 1>);
+      else go(rowreduce_kernel<T, 2, true, false, 1>);
+    }
   }
   *rc = check_launch("rowreduce_kernel");
   return true;
@@ -1291,6 +1304,11 @@ int launch_generic(const bgx_generic_desc &d0, int64_t n_out, int64_t red, cudaS
     if (!no_rr && try_chain_general<T>(d, n_out, red, s, &rc)) return rc;
     if (!no_rr && try_rowreduce<T>(d, n_out, s, &rc)) return rc;
     if (!no_rr && try_chain_general_wide<T>(d, n_out, red, s, &rc)) return rc;
+  } else {
+    // bf16 / f16 storage folded in f32: the staged row kernel (16-byte rows)
+    int rc = 0;
+    static const bool no_rr = getenv("BGX_NO_ROWREDUCE") != nullptr;
+    if (!no_rr && try_rowreduce<T, S>(d, n_out, s, &rc)) return rc;
   }
   if (dense && d.n_in >= 2 && d.n_in <= 3 && red == 1) {
     bool aligned = ((uintptr_t)d.out % 16 == 0) && ((uintptr_t)d.c0 % 16 == 0);

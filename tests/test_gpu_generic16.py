@@ -108,3 +108,27 @@ def test_16bit_prereduced_private_axes_accuracy(dev, text, ext):
     want = torch.einsum(eq, *[x.double() for x in xs])
     err = ((got - want).abs().max() / want.abs().max()).item()
     assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(i,k)->(i)", dict(i=300, k=517)),                  # ragged tiles, thin rows
+    ("(i,k),(k)->(i)", dict(i=5000, k=200)),             # broadcast vector, 4-warp blocks
+    ("(i,k),(i,k)->(i)", dict(i=64, k=1000)),
+    ("(c,a,b)->(a,c)", dict(a=16, c=40, b=64)),          # transposed output rows
+    ("(i,k),(i)->(i)", dict(i=700, k=96)),               # per-row factor (invariant operand)
+])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_16bit_rows_on_staged_kernel_bit_exact(dev, text, ext, dtype):
+    """16-bit row reductions now run on the staged row kernel (16-byte
+    rows, f32 fold): still the reference's sequential order on the widened
+    values with one final rounding — bit-equal to the oracle on f32-widened
+    inputs, c0 included."""
+    s = E.parse_einsum(text)
+    g = torch.Generator().manual_seed(47)
+    xs = [torch.randn([ext[a] for a in t], generator=g).to(dtype) for t in s.inputs]
+    c0 = torch.randn([ext[a] for a in s.output], generator=g).to(dtype)
+    want = np.asarray(oracle.generic(s.inputs, s.output, [x.float().numpy() for x in xs],
+                                     c0.float().numpy()))
+    want16 = torch.from_numpy(want.astype(np.float32)).to(dtype)
+    got = contract(text, *[x.to(dev) for x in xs], c0=c0.to(dev)).cpu()
+    assert torch.equal(got.view(torch.int16), want16.view(torch.int16)), text
