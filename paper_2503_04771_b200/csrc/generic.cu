@@ -702,10 +702,10 @@ rowreduce_kernel(const bgx_generic_desc d, int64_t n_out, uint32_t shared_mask) 
 // operand k is shared by the 32 columns (the vector of a GEMV): one element
 // per lane per tile, read back as a broadcast.
 
-template <typename T, int NIN, int SHM, int ST, int CPW>
+template <typename T, int NIN, int SHM, int ST, int CPW, typename S = T>
 __global__ void __launch_bounds__(32)
 colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
-  constexpr int E16 = 16 / (int)sizeof(T);
+  constexpr int E16 = 16 / (int)sizeof(S);
   constexpr int GPR = CPW / E16;             // 16-byte groups per tile row
   static_assert(GPR >= 1 && 32 % GPR == 0, "a tile row is whole 16-byte groups");
   constexpr int RPI = 32 / GPR;              // tile rows per copy instruction
@@ -715,7 +715,7 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
   constexpr int SSZ = NPC * TSZ + (NIN - NPC) * 32;    // one stage
   extern __shared__ __align__(16) uint8_t cc_smem_raw[];
   const int lane = threadIdx.x;
-  T *wst = reinterpret_cast<T *>(cc_smem_raw);
+  S *wst = reinterpret_cast<S *>(cc_smem_raw);
   const int64_t o0 = (int64_t)blockIdx.x * CPW;
   if (o0 >= n_out) return;
   const int64_t o = o0 + lane % CPW;   // lanes >= CPW fold a duplicate chain, never stored
@@ -734,8 +734,8 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
       for (int k = 0; k < NIN; ++k) base[k] += i * d.strides[k][a];
     }
   }
-  const T *const *ins = reinterpret_cast<const T *const *>(d.ins);
-  const T *src[NIN];
+  const S *const *ins = reinterpret_cast<const S *const *>(d.ins);
+  const S *src[NIN];
   int64_t step[NIN];   // source advance per tile
   const int q = lane % GPR, r0 = lane / GPR;
 #pragma unroll
@@ -747,20 +747,20 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
   }
   const int64_t ntiles = (E + 31) / 32;
   auto issue = [&](int64_t t) {
-    T *stg = wst + (int)(t % ST) * SSZ;
+    S *stg = wst + (int)(t % ST) * SSZ;
     const bool full = (t + 1) * 32 <= E;
     int pc = 0, sc = 0;
 #pragma unroll
     for (int k = 0; k < NIN; ++k) {
-      const T *g = src[k] + t * step[k];
+      const S *g = src[k] + t * step[k];
       if ((SHM >> k) & 1) {
-        T *dst = stg + NPC * TSZ + sc * 32 + lane;
+        S *dst = stg + NPC * TSZ + sc * 32 + lane;
         const bool ok = full || t * 32 + lane < E;
-        if constexpr (sizeof(T) == 4) cp_async4(dst, ok ? g : ins[k], ok);
+        if constexpr (sizeof(S) == 4) cp_async4(dst, ok ? g : ins[k], ok);
         else cp_async8(dst, ok ? g : ins[k], ok);
         ++sc;
       } else {
-        T *dst = stg + pc * TSZ + r0 * RS + q * E16;
+        S *dst = stg + pc * TSZ + r0 * RS + q * E16;
         const int64_t rstep = RPI * d.strides[k][ax];
         if (full) {
 #pragma unroll
@@ -777,7 +777,7 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
     }
     cp_async_commit();
   };
-  T acc = d.c0 ? static_cast<const T *>(d.c0)[o] : T(0);
+  T acc = d.c0 ? ld_as<S, T>(static_cast<const S *>(d.c0) + o) : T(0);
   // (reading a full tile into registers and refilling its stage before the
   // add chain, to issue in the chain's shadow, was 10-15 % slower)
   for (int64_t t = 0; t < ST - 1; ++t) {
@@ -787,8 +787,8 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
     if (t + ST - 1 < ntiles) issue(t + ST - 1); else cp_async_commit();
     cp_async_wait<ST - 1>();
     __syncwarp();
-    const T *stg = wst + (int)(t % ST) * SSZ;
-    const T *col[NIN];
+    const S *stg = wst + (int)(t % ST) * SSZ;
+    const S *col[NIN];
     {
       int pc = 0, sc = 0;
 #pragma unroll
@@ -797,7 +797,9 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
         else col[k] = stg + (pc++) * TSZ + lane % CPW;
       }
     }
-    auto elem = [&](int k, int c) { return ((SHM >> k) & 1) ? col[k][c] : col[k][c * RS]; };
+    auto elem = [&](int k, int c) {
+      return ld_as<S, T>(((SHM >> k) & 1) ? col[k] + c : col[k] + c * RS);
+    };
     if ((t + 1) * 32 <= E) {
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
@@ -818,7 +820,7 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
     __syncwarp();
   }
   cp_async_wait<0>();
-  if (lane < CPW) static_cast<T *>(d.out)[o] = acc;
+  if (lane < CPW) static_cast<S *>(d.out)[o] = st_as<S, T>(acc);
 }
 
 // Column chains (colchain_kernel) when every warp's 32 (or 8) outputs are
@@ -830,7 +832,7 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
 // the block-per-output chain kernels.  BGX_NO_COLCHAIN=1 for A/B.
 constexpr int64_t CC_MIN_OUT = 512;
 
-template <typename T>
+template <typename T, typename S = T>
 bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int *rc) {
   static const bool off = getenv("BGX_NO_COLCHAIN") != nullptr;
   const int ax = d.n_axes - 1, inner = d.n_par - 1;
@@ -841,12 +843,13 @@ bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int 
   for (int k = 0; k < d.n_in; ++k) {
     if (d.strides[k][inner] == 0) { shm |= 1 << k; continue; }
     if (d.strides[k][inner] != 1 || ((uintptr_t)d.ins[k] % 16) != 0 ||
-        (d.strides[k][ax] * (int64_t)sizeof(T)) % 16 != 0)
+        (d.strides[k][ax] * (int64_t)sizeof(S)) % 16 != 0)
       return false;
     for (int a = 0; a < inner; ++a)
-      if (d.extents[a] > 1 && (d.strides[k][a] * (int64_t)sizeof(T)) % 16 != 0) return false;
+      if (d.extents[a] > 1 && (d.strides[k][a] * (int64_t)sizeof(S)) % 16 != 0) return false;
   }
   if (shm == (1 << d.n_in) - 1) return false;
+  if (sizeof(S) == 2 && shm != 0) return false;   // 16-bit: per-column operands only
   // one warp per block (4-warp blocks: 10-40 % slower, scripts/r02/rr_vcols_ab.sh).
   // A warp's chains advance one tile per ~500 cycles whatever the pipeline
   // depth, so with fewer 32-column groups than SMs the columns are split 8 per
@@ -857,19 +860,21 @@ bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int 
   if (n_out % cpw || d.extents[inner] % cpw) return false;
   const int64_t warps = n_out / cpw;
   const int st = warps >= 2 * sms ? 4 : 8;
-  constexpr int E16 = 16 / (int)sizeof(T);
+  constexpr int E16 = 16 / (int)sizeof(S);
   const int npc = d.n_in - __builtin_popcount(shm);
-  const size_t smem = (size_t)st * (npc * 32 * (cpw + E16) + (d.n_in - npc) * 32) * sizeof(T);
+  const size_t smem = (size_t)st * (npc * 32 * (cpw + E16) + (d.n_in - npc) * 32) * sizeof(S);
   auto go = [&](auto kern) {
     set_max_smem_once(reinterpret_cast<const void *>(kern), 200 * 1024);
     kern<<<(unsigned)warps, 32, smem, s>>>(d, n_out);
   };
   auto pick = [&](auto stc, auto cpwc) {
     constexpr int ST = decltype(stc)::value, CPW = decltype(cpwc)::value;
-    if (d.n_in == 1) go(colchain_kernel<T, 1, 0, ST, CPW>);
-    else if (shm == 0) go(colchain_kernel<T, 2, 0, ST, CPW>);
-    else if (shm == 1) go(colchain_kernel<T, 2, 1, ST, CPW>);
-    else go(colchain_kernel<T, 2, 2, ST, CPW>);
+    if (d.n_in == 1) go(colchain_kernel<T, 1, 0, ST, CPW, S>);
+    else if (shm == 0) go(colchain_kernel<T, 2, 0, ST, CPW, S>);
+    else if constexpr (sizeof(S) != 2) {
+      if (shm == 1) go(colchain_kernel<T, 2, 1, ST, CPW, S>);
+      else go(colchain_kernel<T, 2, 2, ST, CPW, S>);
+    }
   };
   using I4 = std::integral_constant<int, 4>;
   using I8 = std::integral_constant<int, 8>;
@@ -887,9 +892,7 @@ bool try_rowreduce(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int
   constexpr bool same = std::is_same<S, T>::value;
   if (d.n_axes != d.n_par + 1 || d.n_in < 1 || d.n_in > 2 || d.n_par < 1) return false;
   const int ax = d.n_axes - 1, inner = d.n_par - 1;
-  if constexpr (same) {
-    if (try_colchain<T>(d, n_out, s, rc)) return true;
-  }
+  if (try_colchain<T, S>(d, n_out, s, rc)) return true;
   bool rows = true, cols = true;
   // rows mode may carry operands constant along the reduction (a per-output
   // factor, loaded once per lane) as long as one operand streams the row

@@ -132,3 +132,24 @@ def test_16bit_rows_on_staged_kernel_bit_exact(dev, text, ext, dtype):
     want16 = torch.from_numpy(want.astype(np.float32)).to(dtype)
     got = contract(text, *[x.to(dev) for x in xs], c0=c0.to(dev)).cpu()
     assert torch.equal(got.view(torch.int16), want16.view(torch.int16)), text
+
+
+@pytest.mark.parametrize("text,ext", [
+    ("(k,i)->(i)", dict(k=300, i=8192)),            # 32 columns per warp, ragged tile
+    ("(k,i),(k,i)->(i)", dict(k=100, i=1024)),      # 8 columns per warp
+    ("(a,b,d)->(b,d)", dict(a=64, b=32, d=64)),
+])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_16bit_columns_on_staged_kernel_bit_exact(dev, text, ext, dtype):
+    """16-bit column reductions with per-column operands run on the staged
+    column-chain kernel (16-byte copies, f32 fold, one rounding): bit-equal
+    to the oracle on f32-widened inputs, c0 included."""
+    s = E.parse_einsum(text)
+    g = torch.Generator().manual_seed(53)
+    xs = [torch.randn([ext[a] for a in t], generator=g).to(dtype) for t in s.inputs]
+    c0 = torch.randn([ext[a] for a in s.output], generator=g).to(dtype)
+    want = np.asarray(oracle.generic(s.inputs, s.output, [x.float().numpy() for x in xs],
+                                     c0.float().numpy()))
+    want16 = torch.from_numpy(want.astype(np.float32)).to(dtype)
+    got = contract(text, *[x.to(dev) for x in xs], c0=c0.to(dev)).cpu()
+    assert torch.equal(got.view(torch.int16), want16.view(torch.int16)), text
