@@ -754,10 +754,19 @@ colchain_kernel(const bgx_generic_desc d, int64_t n_out) {
     for (int k = 0; k < NIN; ++k) {
       const S *g = src[k] + t * step[k];
       if ((SHM >> k) & 1) {
-        S *dst = stg + NPC * TSZ + sc * 32 + lane;
-        const bool ok = full || t * 32 + lane < E;
-        if constexpr (sizeof(S) == 4) cp_async4(dst, ok ? g : ins[k], ok);
-        else cp_async8(dst, ok ? g : ins[k], ok);
+        if constexpr (sizeof(S) == 2) {
+          // 16-bit shared operand (unit stride, 16-byte aligned: host-checked):
+          // lanes 0-3 copy the tile's 32 values as 4 x 16 bytes
+          S *dst = stg + NPC * TSZ + sc * 32 + lane * 8;
+          const int64_t left = E - t * 32 - lane * 8;
+          const int bytes = left >= 8 ? 16 : (left > 0 ? (int)left * 2 : 0);
+          if (lane < 4) cp_async16(dst, bytes ? g + 7 * lane : ins[k], bytes);
+        } else {
+          S *dst = stg + NPC * TSZ + sc * 32 + lane;
+          const bool ok = full || t * 32 + lane < E;
+          if constexpr (sizeof(S) == 4) cp_async4(dst, ok ? g : ins[k], ok);
+          else cp_async8(dst, ok ? g : ins[k], ok);
+        }
         ++sc;
       } else {
         S *dst = stg + pc * TSZ + r0 * RS + q * E16;
@@ -849,7 +858,16 @@ bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int 
       if (d.extents[a] > 1 && (d.strides[k][a] * (int64_t)sizeof(S)) % 16 != 0) return false;
   }
   if (shm == (1 << d.n_in) - 1) return false;
-  if (sizeof(S) == 2 && shm != 0) return false;   // 16-bit: per-column operands only
+  if (sizeof(S) == 2) {
+    // 16-bit shared operands are staged 16 bytes at a time: unit stride along
+    // the reduction, 16-byte aligned for every warp
+    for (int k = 0; k < d.n_in; ++k) {
+      if (!((shm >> k) & 1)) continue;
+      if (d.strides[k][ax] != 1 || ((uintptr_t)d.ins[k] % 16) != 0) return false;
+      for (int a = 0; a < inner; ++a)
+        if (d.extents[a] > 1 && (d.strides[k][a] * 2) % 16 != 0) return false;
+    }
+  }
   // one warp per block (4-warp blocks: 10-40 % slower, scripts/r02/rr_vcols_ab.sh).
   // A warp's chains advance one tile per ~500 cycles whatever the pipeline
   // depth, so with fewer 32-column groups than SMs the columns are split 8 per
@@ -871,10 +889,8 @@ bool try_colchain(const bgx_generic_desc &d, int64_t n_out, cudaStream_t s, int 
     constexpr int ST = decltype(stc)::value, CPW = decltype(cpwc)::value;
     if (d.n_in == 1) go(colchain_kernel<T, 1, 0, ST, CPW, S>);
     else if (shm == 0) go(colchain_kernel<T, 2, 0, ST, CPW, S>);
-    else if constexpr (sizeof(S) != 2) {
-      if (shm == 1) go(colchain_kernel<T, 2, 1, ST, CPW, S>);
-      else go(colchain_kernel<T, 2, 2, ST, CPW, S>);
-    }
+    else if (shm == 1) go(colchain_kernel<T, 2, 1, ST, CPW, S>);
+    else go(colchain_kernel<T, 2, 2, ST, CPW, S>);
   };
   using I4 = std::integral_constant<int, 4>;
   using I8 = std::integral_constant<int, 8>;

@@ -8,3 +8,8 @@ for env in "BGX_NO_COLCHAIN=1" "BGX_X=1"; do
   env $env $P "(k,i),(k)->(i)" k=8192,i=8192
   env $env $P "(i,k)->(k)" i=8192,k=8192
 done
+for env in "BGX_NO_COLCHAIN=1" "BGX_X=1"; do
+  echo "== shared vector, $env"
+  env $env $P "(k,i),(k)->(i)" k=768,i=32768 auto bfloat16
+  env $env $P "(b,k,i),(b,k)->(b,i)" b=64,k=512,i=1024 auto bfloat16
+done

@@ -138,6 +138,9 @@ def test_16bit_rows_on_staged_kernel_bit_exact(dev, text, ext, dtype):
     ("(k,i)->(i)", dict(k=300, i=8192)),            # 32 columns per warp, ragged tile
     ("(k,i),(k,i)->(i)", dict(k=100, i=1024)),      # 8 columns per warp
     ("(a,b,d)->(b,d)", dict(a=64, b=32, d=64)),
+    ("(k,i),(k)->(i)", dict(k=300, i=2048)),        # shared vector, 16-byte staged
+    ("(k),(k,i)->(i)", dict(k=77, i=1024)),         # shared operand first, ragged tail
+    ("(b,k,i),(b,k)->(b,i)", dict(b=3, k=200, i=512)),  # shared within a warp only
 ])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_16bit_columns_on_staged_kernel_bit_exact(dev, text, ext, dtype):
